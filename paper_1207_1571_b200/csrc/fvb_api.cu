@@ -1,0 +1,1168 @@
+// libfvb C ABI: context lifetime, one-time uploads of the mesh, pattern and
+// boundary tables, single-operator entry points (host buffers in/out) and
+// the device-resident PISO step / SIMPLE sweep (coupling.py:216-370).
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fvb_internal.cuh"
+
+static thread_local std::string g_last_error;
+
+void fvb_set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+using namespace fvb;
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// temporary device buffer for the operator entry points
+struct Tmp {
+  void* p = nullptr;
+  ~Tmp() {
+    if (p) cudaFree(p);
+  }
+};
+
+template <typename T>
+int tmp_upload(Ctx* c, Tmp& t, const T* host, size_t n, T** out) {
+  FVB_CUDA(cudaMalloc(&t.p, (n ? n : 1) * sizeof(T)));
+  if (host && n) FVB_CUDA(cudaMemcpyAsync(t.p, host, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  *out = static_cast<T*>(t.p);
+  return FVB_OK;
+}
+
+template <typename T>
+int tmp_zero(Ctx* c, Tmp& t, size_t n, T** out) {
+  FVB_CUDA(cudaMalloc(&t.p, (n ? n : 1) * sizeof(T)));
+  FVB_CUDA(cudaMemsetAsync(t.p, 0, (n ? n : 1) * sizeof(T), c->stream));
+  *out = static_cast<T*>(t.p);
+  return FVB_OK;
+}
+
+template <typename T>
+int d2h(Ctx* c, T* host, const T* dev, size_t n) {
+  if (n) FVB_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  return FVB_OK;
+}
+
+template <typename T>
+int h2d(Ctx* c, T* dev, const T* host, size_t n) {
+  if (n) FVB_CUDA(cudaMemcpyAsync(dev, host, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  return FVB_OK;
+}
+
+int sync(Ctx* c) {
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  return FVB_OK;
+}
+
+// row-major (n,k) <-> slot-major [k*n]
+std::vector<double> to_slot_major(const double* V, int n, int k) {
+  std::vector<double> o(size_t(n) * k);
+  for (int i = 0; i < n; ++i)
+    for (int s = 0; s < k; ++s) o[size_t(s) * n + i] = V[size_t(i) * k + s];
+  return o;
+}
+void from_slot_major(const std::vector<double>& o, double* V, int n, int k) {
+  for (int i = 0; i < n; ++i)
+    for (int s = 0; s < k; ++s) V[size_t(i) * k + s] = o[size_t(s) * n + i];
+}
+
+struct DevMatrix {
+  Tmp tv, tc;
+  MatView m{nullptr, nullptr};
+};
+
+int upload_matrix(Ctx* c, DevMatrix& M, const double* V, const double* crs) {
+  std::vector<double> sm = to_slot_major(V, c->nc, c->k);
+  double* dv;
+  double* dc;
+  FVB_TRY(tmp_upload(c, M.tv, sm.data(), sm.size(), &dv));
+  FVB_TRY(tmp_upload(c, M.tc, crs, size_t(c->nnz_crs), &dc));
+  M.m = MatView{dv, dc};
+  return sync(c);
+}
+
+int download_matrix(Ctx* c, DevMatrix& M, double* V, double* crs) {
+  std::vector<double> sm(size_t(c->nc) * c->k);
+  FVB_TRY(d2h(c, sm.data(), M.m.V, sm.size()));
+  if (crs) FVB_TRY(d2h(c, crs, M.m.crs, size_t(c->nnz_crs)));
+  FVB_TRY(sync(c));
+  from_slot_major(sm, V, c->nc, c->k);
+  return FVB_OK;
+}
+
+int need_mesh(Ctx* c) {
+  if (!c->have_mesh) {
+    fvb_set_error("no mesh uploaded to this context");
+    return FVB_E_ARG;
+  }
+  return FVB_OK;
+}
+int need_pattern(Ctx* c) {
+  if (!c->have_pattern) {
+    fvb_set_error("no pattern uploaded to this context");
+    return FVB_E_ARG;
+  }
+  return FVB_OK;
+}
+int need_bc(Ctx* c, int field) {
+  if (field < 0 || field > 1 || !c->have_bc[field]) {
+    fvb_set_error("boundary conditions of field %d not set", field);
+    return FVB_E_ARG;
+  }
+  return FVB_OK;
+}
+
+// ---------------------------------------------------------------- kernels
+__global__ void k_fill(double* a, size_t n, double v) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+       i += size_t(gridDim.x) * blockDim.x)
+    a[i] = v;
+}
+
+__global__ void k_get_diag(int n, const int* ds, const double* V, double* diag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    diag[i] = V[size_t(ds[i]) * n + i];
+}
+
+__global__ void k_set_diag(int n, const int* ds, double* V, const double* diag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    V[size_t(ds[i]) * n + i] = diag[i];
+}
+
+// rhs = b0 - V grad p   (coupling.py:253); SIMPLE implicit relaxation
+// (coupling.py:254-258): V[diag] = diag/alpha, rhs += (scaled - diag) u
+__global__ void k_mom_rhs(int n, const double* b0, const double* vol, const double* gp,
+                          const double* diag, const double* u, double* rhs, double* V,
+                          const int* ds, int relax, double alpha_u) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = vol[i];
+    double scaled = 0.0;
+    if (relax) {
+      scaled = diag[i] / alpha_u;
+      V[size_t(ds[i]) * n + i] = scaled;
+    }
+    for (int c = 0; c < 3; ++c) {
+      double r = b0[size_t(c) * n + i] - v * gp[size_t(c) * n + i];
+      if (relax) r = r + (scaled - diag[i]) * u[size_t(c) * n + i];
+      rhs[size_t(c) * n + i] = r;
+    }
+  }
+}
+
+// per-block sum of squares of up to 3 arrays (partials, fixed order)
+__global__ void k_sumsq(int n, int ncomp, const double* x, double* partials) {
+  __shared__ double red[32 * 3];
+  double acc[3] = {0.0, 0.0, 0.0};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int c = 0; c < ncomp; ++c) {
+      const double v = x[size_t(c) * n + i];
+      acc[c] += v * v;
+    }
+  block_reduce<3>(acc, red);
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 3; ++c) partials[size_t(c) * gridDim.x + blockIdx.x] = acc[c];
+}
+
+__global__ void k_absmax(int n, const double* x, double* partials) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    m = fmax(m, fabs(x[i]));
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) partials[blockIdx.x] = m;
+  }
+}
+
+// HbyA = u + (b0 - A u)/a_P  (coupling.py:290-291); rAU = V/a_P (301)
+__global__ void k_hbya(int n, const double* u, const double* b0, const double* au,
+                       const double* diag, const double* vol, double* hv, double* rau) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double d = diag[i];
+    for (int c = 0; c < 3; ++c) {
+      const size_t k = size_t(c) * n + i;
+      hv[k] = u[k] + (b0[k] - au[k]) / d;
+    }
+    rau[i] = vol[i] / d;
+  }
+}
+
+// rhs = rhs_L - div(phiHbyA); pin the reference cell (coupling.py:314-319)
+__global__ void k_p_rhs(int n, const double* rl, const double* divh, double* rhs) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    rhs[i] = rl[i] - divh[i];
+}
+__global__ void k_pin(int n, const int* ds, double* V, double* rhs, int ref, double pref) {
+  const double dref = V[size_t(ds[ref]) * n + ref];
+  rhs[ref] += dref * pref;
+  V[size_t(ds[ref]) * n + ref] = 2.0 * dref;
+}
+
+// flux = phiHbyA - laplacian_face_flux (coupling.py:334)
+__global__ void k_flux_corr(int nf, const double* phih, const double* lf, double* flux) {
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x)
+    flux[f] = phih[f] - lf[f];
+}
+
+// p = p_before + alpha_p (p - p_before)  (coupling.py:335-336)
+__global__ void k_relax_p(int n, double* p, const double* pb, double a) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = pb[i] + a * (p[i] - pb[i]);
+}
+
+// u = HbyA - rAU grad p  (coupling.py:341)
+__global__ void k_u_corr(int n, const double* hv, const double* rau, const double* gp, double* u) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int c = 0; c < 3; ++c) u[size_t(c) * n + i] = hv[size_t(c) * n + i] - rau[i] * gp[size_t(c) * n + i];
+}
+
+int fill(Ctx* c, double* a, size_t n, double v) {
+  k_fill<<<grid_for(int64_t(n), kThreads), kThreads, 0, c->stream>>>(a, n, v);
+  FVB_CUDA(cudaGetLastError());
+  return FVB_OK;
+}
+
+int sumsq(Ctx* c, int ncomp, const double* x, double* out) {
+  const int blocks = 2 * c->num_sms;
+  k_sumsq<<<blocks, kThreads, 0, c->stream>>>(c->nc, ncomp, x, c->partials);
+  FVB_CUDA(cudaGetLastError());
+  std::vector<double> h(3 * size_t(blocks));
+  FVB_TRY(d2h(c, h.data(), c->partials, h.size()));
+  FVB_TRY(sync(c));
+  for (int k = 0; k < ncomp; ++k) {
+    double s = 0.0;
+    for (int b = 0; b < blocks; ++b) s += h[size_t(k) * blocks + b];
+    out[k] = s;
+  }
+  return FVB_OK;
+}
+
+// ----------------------------------------------------------- step state
+struct StepWork {
+  bool ready = false;
+  double *Vm, *crsm, *b0, *diag, *rhs, *gu, *gp, *hv, *au, *phih, *divh, *rau, *rauf, *Vp, *crsp,
+      *rl, *rp, *coef, *corr, *lf, *pbefore;
+};
+
+StepWork& work_of(Ctx* c);
+
+int ensure_work(Ctx* c) {
+  StepWork& w = work_of(c);
+  if (w.ready) return FVB_OK;
+  const size_t n = c->nc, nf = c->nf, kn = size_t(c->k) * n, nz = size_t(c->nnz_crs);
+  FVB_TRY(dalloc(c, &w.Vm, kn));
+  FVB_TRY(dalloc(c, &w.crsm, nz));
+  FVB_TRY(dalloc(c, &w.b0, 3 * n));
+  FVB_TRY(dalloc(c, &w.diag, n));
+  FVB_TRY(dalloc(c, &w.rhs, 3 * n));
+  FVB_TRY(dalloc(c, &w.gu, 9 * n));
+  FVB_TRY(dalloc(c, &w.gp, 3 * n));
+  FVB_TRY(dalloc(c, &w.hv, 3 * n));
+  FVB_TRY(dalloc(c, &w.au, 3 * n));
+  FVB_TRY(dalloc(c, &w.phih, nf));
+  FVB_TRY(dalloc(c, &w.divh, n));
+  FVB_TRY(dalloc(c, &w.rau, n));
+  FVB_TRY(dalloc(c, &w.rauf, nf));
+  FVB_TRY(dalloc(c, &w.Vp, kn));
+  FVB_TRY(dalloc(c, &w.crsp, nz));
+  FVB_TRY(dalloc(c, &w.rl, n));
+  FVB_TRY(dalloc(c, &w.rp, n));
+  FVB_TRY(dalloc(c, &w.coef, nf));
+  FVB_TRY(dalloc(c, &w.corr, nf));
+  FVB_TRY(dalloc(c, &w.lf, nf));
+  FVB_TRY(dalloc(c, &w.pbefore, n));
+  w.ready = true;
+  return FVB_OK;
+}
+
+struct CtxExt {
+  StepWork work;
+};
+std::vector<std::pair<Ctx*, CtxExt*>> g_ext;
+
+StepWork& work_of(Ctx* c) {
+  for (auto& e : g_ext)
+    if (e.first == c) return e.second->work;
+  g_ext.push_back({c, new CtxExt()});
+  return g_ext.back().second->work;
+}
+
+void drop_ext(Ctx* c) {
+  for (size_t i = 0; i < g_ext.size(); ++i)
+    if (g_ext[i].first == c) {
+      delete g_ext[i].second;
+      g_ext.erase(g_ext.begin() + i);
+      return;
+    }
+}
+
+void fill_report(fvb_solve_report& r, const SolveOut& o) {
+  r.iterations = o.iterations;
+  r.converged = o.converged;
+  r.initial_residual = o.res0;
+  r.final_residual = o.res;
+  r.wall_time = 0.0;
+  r.error_iteration = o.error_iteration;
+  r.error_kind = o.error_kind;
+}
+
+int log_solve(fvb_step_report* rep, int solver, int field, const SolveOut& o) {
+  if (rep->n_solves >= FVB_MAX_SOLVES) {
+    fvb_set_error("too many solves in one step");
+    return FVB_E_ARG;
+  }
+  const int k = rep->n_solves++;
+  rep->solver[k] = solver;
+  rep->field[k] = field;
+  fill_report(rep->rep[k], o);
+  return FVB_OK;
+}
+
+float ev_ms(Ctx* c, int a, int b) {
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->ev[a], c->ev[b]);
+  return ms;
+}
+
+// _momentum_matrix (coupling.py:216-231)
+int momentum_matrix(Ctx* c, const fvb_step_cfg* cfg, bool with_ddt) {
+  StepWork& w = work_of(c);
+  const size_t n = c->nc;
+  MatView Am{w.Vm, w.crsm};
+  FVB_CUDA(cudaMemsetAsync(w.Vm, 0, sizeof(double) * c->k * n, c->stream));
+  if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsm, 0, sizeof(double) * c->nnz_crs, c->stream));
+  FVB_CUDA(cudaMemsetAsync(w.b0, 0, sizeof(double) * 3 * n, c->stream));
+  if (with_ddt) FVB_TRY(op_ddt(c, 3, Am, w.b0, c->u, cfg->dt, 1.0));
+  FVB_TRY(op_convection(c, 0, 3, Am, w.b0, c->flux, c->ub, cfg->scheme, 1.0));
+  const bool corr = cfg->nonorth_correction && cfg->limiter > 0.0;
+  if (corr) FVB_TRY(op_gradient(c, 0, 3, c->u, c->ub, w.gu));
+  FVB_TRY(op_laplacian(c, 0, 3, Am, w.b0, cfg->nu, nullptr, c->u, c->ub, w.gu,
+                       cfg->nonorth_correction, cfg->limiter, -1.0, nullptr, nullptr));
+  return FVB_OK;
+}
+
+// _solve_momentum (coupling.py:234-279); returns worst normalised residual
+int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report* rep) {
+  StepWork& w = work_of(c);
+  const int n = c->nc;
+  const int g = grid_for(n, kThreads);
+  k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag);
+  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
+  const bool relaxing = relax && cfg->alpha_u < 1.0;
+  k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, w.b0, c->vol, w.gp, w.diag, c->u, w.rhs, w.Vm,
+                                           c->diag_slot, relaxing, cfg->alpha_u);
+  FVB_CUDA(cudaGetLastError());
+  double bn2[3];
+  FVB_TRY(sumsq(c, 3, w.rhs, bn2));
+  double bn[3], bscale = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    bn[k] = std::sqrt(bn2[k]);
+    bscale = std::max(bscale, bn[k]);
+  }
+  bscale = std::max(bscale, 1e-30);
+  FVB_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  const double* b[3] = {w.rhs, w.rhs + n, w.rhs + 2 * size_t(n)};
+  double* x[3] = {c->u, c->u + n, c->u + 2 * size_t(n)};
+  SolveOut out[3];
+  FVB_TRY(bicgstab_solve(c, MatView{w.Vm, w.crsm}, 3, b, x, cfg->mom_tol, cfg->mom_abs_tol,
+                         cfg->mom_max_iters, out));
+  FVB_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  static const char* names[3] = {"ux", "uy", "uz"};
+  double worst = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    if (out[k].error_kind != SE_NONE) {
+      rep->failed_solve = rep->n_solves;
+      std::string msg = solve_error_text("bicgstab", out[k], out[k].error_iteration);
+      fvb_set_error("momentum solve for %s failed at outer {outer}: %s", names[k], msg.c_str());
+      return out[k].error_kind == SE_TIMEOUT ? FVB_E_TIMEOUT : FVB_E_COUPLING;
+    }
+    FVB_TRY(log_solve(rep, 1, k, out[k]));
+    rep->rep[rep->n_solves - 1].wall_time = ev_ms(c, 2, 3) * 1e-3;
+    worst = std::max(worst, out[k].res0 * bn[k] / bscale);
+  }
+  if (relaxing) {
+    k_set_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag);
+    FVB_CUDA(cudaGetLastError());
+  }
+  rep->mom_res = worst;
+  return FVB_OK;
+}
+
+// _pressure_correct (coupling.py:282-344)
+int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_report* rep,
+                     double* first_res, double* t_asm, double* t_solve, double* t_corr) {
+  StepWork& w = work_of(c);
+  const int n = c->nc;
+  const int g = grid_for(n, kThreads);
+  FVB_CUDA(cudaEventRecord(c->ev[4], c->stream));
+  MatView Am{w.Vm, w.crsm};
+  for (int k = 0; k < 3; ++k) FVB_TRY(smvp(c, Am, c->u + size_t(k) * n, w.au + size_t(k) * n));
+  k_hbya<<<g, kThreads, 0, c->stream>>>(n, c->u, w.b0, w.au, w.diag, c->vol, w.hv, w.rau);
+  FVB_CUDA(cudaGetLastError());
+  FVB_TRY(op_face_flux(c, 3, w.hv, c->ub, 0, w.phih));
+  FVB_TRY(op_divergence(c, w.phih, w.divh));
+  FVB_TRY(op_interp(c, -1, 1, w.rau, nullptr, w.rauf));
+  if (relax_p) FVB_CUDA(cudaMemcpyAsync(w.pbefore, c->p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  FVB_CUDA(cudaEventRecord(c->ev[5], c->stream));
+  float asm_ms = 0.f, solve_ms = 0.f;
+  const bool corr = cfg->nonorth_correction && cfg->limiter > 0.0;
+  MatView Ap{w.Vp, w.crsp};
+  for (int it = 0; it <= cfg->n_nonorth_correctors; ++it) {
+    FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
+    FVB_CUDA(cudaMemsetAsync(w.Vp, 0, sizeof(double) * c->k * size_t(n), c->stream));
+    if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsp, 0, sizeof(double) * c->nnz_crs, c->stream));
+    FVB_CUDA(cudaMemsetAsync(w.rl, 0, sizeof(double) * n, c->stream));
+    if (corr) FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
+    FVB_TRY(op_laplacian(c, 1, 1, Ap, w.rl, 0.0, w.rauf, c->p, c->pb, w.gp,
+                         cfg->nonorth_correction, cfg->limiter, -1.0, w.coef, w.corr));
+    k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, w.rl, w.divh, w.rp);
+    if (cfg->pin_pressure)
+      k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, w.rp, cfg->pressure_ref_cell,
+                                    cfg->pressure_ref_value);
+    FVB_CUDA(cudaGetLastError());
+    FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
+    SolveOut o;
+    FVB_TRY(cg_solve(c, Ap, w.rp, c->p, cfg->p_tol, cfg->p_abs_tol, cfg->p_max_iters, &o));
+    asm_ms += ev_ms(c, 6, 7);
+    FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
+    FVB_CUDA(cudaEventSynchronize(c->ev[6]));
+    const float this_solve = ev_ms(c, 7, 6);
+    solve_ms += this_solve;
+    if (o.error_kind != SE_NONE) {
+      rep->failed_solve = rep->n_solves;
+      std::string msg = solve_error_text("cg", o, o.error_iteration);
+      fvb_set_error("pressure solve failed at outer {outer}: %s", msg.c_str());
+      return o.error_kind == SE_TIMEOUT ? FVB_E_TIMEOUT : FVB_E_COUPLING;
+    }
+    FVB_TRY(log_solve(rep, 0, 3, o));
+    rep->rep[rep->n_solves - 1].wall_time = this_solve * 1e-3;
+    if (*first_res < 0) *first_res = o.res0;
+  }
+  FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
+  FVB_TRY(op_lap_flux(c, 1, 1, w.coef, w.corr, c->p, c->pb, w.lf));
+  k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux);
+  if (relax_p && cfg->alpha_p < 1.0)
+    k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, w.pbefore, cfg->alpha_p);
+  FVB_CUDA(cudaGetLastError());
+  FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
+  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
+  k_u_corr<<<g, kThreads, 0, c->stream>>>(n, w.hv, w.rau, w.gp, c->u);
+  FVB_CUDA(cudaGetLastError());
+  FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
+  FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
+  FVB_CUDA(cudaEventSynchronize(c->ev[7]));
+  *t_asm += (ev_ms(c, 4, 5) + asm_ms) * 1e-3;
+  *t_solve += solve_ms * 1e-3;
+  *t_corr += ev_ms(c, 6, 7) * 1e-3;
+  return FVB_OK;
+}
+
+int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_report* rep,
+             bool piso) {
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_pattern(c));
+  FVB_TRY(need_bc(c, 0));
+  FVB_TRY(need_bc(c, 1));
+  FVB_TRY(ensure_work(c));
+  memset(rep, 0, sizeof(*rep));
+  rep->failed_solve = -1;
+  rep->p_res = -1.0;
+  if (c->n_patches[0] && speeds)
+    FVB_TRY(h2d(c, c->bc_speed[0], speeds, size_t(c->n_patches[0])));
+  FVB_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  if (piso) {  // piso_time_step applies BCs at the new time first (coupling.py:360-361)
+    FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
+    FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
+  }
+  FVB_TRY(momentum_matrix(c, cfg, piso));
+  FVB_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  FVB_TRY(solve_momentum(c, cfg, !piso, rep));
+  FVB_CUDA(cudaEventSynchronize(c->ev[3]));
+  rep->t_momentum_assembly = ev_ms(c, 0, 1) * 1e-3;
+  rep->t_momentum_solve = ev_ms(c, 2, 3) * 1e-3;
+  double first = -1.0;
+  const int ncorr = piso ? cfg->n_correctors : 1;
+  for (int k = 0; k < ncorr; ++k)
+    FVB_TRY(pressure_correct(c, cfg, !piso, rep, &first, &rep->t_pressure_assembly,
+                             &rep->t_pressure_solve, &rep->t_correction));
+  rep->p_res = first;
+  return FVB_OK;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+extern "C" {
+
+int fvb_version(void) { return 100; }
+const char* fvb_last_error(void) { return g_last_error.c_str(); }
+int fvb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int fvb_ctx_create(int device, fvb_ctx** out) {
+  auto* h = new fvb_ctx();
+  Ctx* c = &h->c;
+  c->dev = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    fvb_set_error("cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+    delete h;
+    return FVB_E_CUDA;
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    fvb_set_error("stream creation failed");
+    delete h;
+    return FVB_E_CUDA;
+  }
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  for (auto& ev : c->tev) cudaEventCreate(&ev);
+  int rc = dalloc(c, &c->sync, 64);
+  if (!rc) rc = dalloc(c, &c->partials, 16 * 4096 + 256);
+  if (!rc) rc = dalloc(c, &c->ipart, 64);
+  if (rc) {
+    fvb_ctx_destroy(h);
+    return rc;
+  }
+  cudaMemset(c->sync, 0, 64 * sizeof(unsigned));
+  *out = h;
+  return FVB_OK;
+}
+
+int fvb_ctx_destroy(fvb_ctx* h) {
+  if (!h) return FVB_OK;
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : c->allocs) cudaFree(p);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : c->tev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  drop_ext(c);
+  delete h;
+  return FVB_OK;
+}
+
+int64_t fvb_ctx_device_bytes(fvb_ctx* h) { return h ? h->c.bytes : 0; }
+
+int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_internal,
+                    const int64_t* owner, const int64_t* neighbour, const double* sf,
+                    const double* smag, const double* vol, const double* w, const double* d,
+                    const double* db) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  if (c->have_mesh) {
+    fvb_set_error("mesh already uploaded");
+    return FVB_E_ARG;
+  }
+  if (n_cells <= 0 || n_faces < n_internal || n_faces >= (int64_t(1) << 31) ||
+      n_cells >= (int64_t(1) << 31)) {
+    fvb_set_error("mesh sizes out of range");
+    return FVB_E_ARG;
+  }
+  c->nc = int(n_cells);
+  c->nf = int(n_faces);
+  c->ni = int(n_internal);
+  c->nb = c->nf - c->ni;
+  const size_t nc = c->nc, nf = c->nf, ni = c->ni, nb = c->nb;
+  std::vector<int> own(nf), nbr(ni);
+  for (size_t f = 0; f < nf; ++f) {
+    if (owner[f] < 0 || owner[f] >= n_cells) {
+      fvb_set_error("owner cell index out of range");
+      return FVB_E_MESH;
+    }
+    own[f] = int(owner[f]);
+  }
+  for (size_t f = 0; f < ni; ++f) {
+    if (neighbour[f] < 0 || neighbour[f] >= n_cells) {
+      fvb_set_error("neighbour cell index out of range");
+      return FVB_E_MESH;
+    }
+    nbr[f] = int(neighbour[f]);
+  }
+  // per-cell face list: owned faces ascending, then neighbour faces ascending
+  std::vector<int> nown(nc, 0), nnb(nc, 0);
+  for (size_t f = 0; f < nf; ++f) nown[own[f]]++;
+  for (size_t f = 0; f < ni; ++f) nnb[nbr[f]]++;
+  std::vector<int> ptr(nc + 1, 0);
+  for (size_t i = 0; i < nc; ++i) {
+    const int64_t next = int64_t(ptr[i]) + nown[i] + nnb[i];
+    if (next >= (int64_t(1) << 31)) {
+      fvb_set_error("face list too long");
+      return FVB_E_ARG;
+    }
+    ptr[i + 1] = int(next);
+  }
+  std::vector<int> cf(ptr[nc]);
+  std::vector<int> po(nc), pn(nc);
+  for (size_t i = 0; i < nc; ++i) {
+    po[i] = ptr[i];
+    pn[i] = ptr[i] + nown[i];
+  }
+  for (size_t f = 0; f < nf; ++f) cf[po[own[f]]++] = int(f);
+  for (size_t f = 0; f < ni; ++f) cf[pn[nbr[f]]++] = ~int(f);
+  // SoA geometry
+  std::vector<double> tmp(std::max(nf, nc));
+  auto up3 = [&](const double* src, size_t m, double** o0, double** o1, double** o2) -> int {
+    double* outs[3];
+    for (int k = 0; k < 3; ++k) {
+      FVB_TRY(dalloc(c, &outs[k], m));
+      for (size_t i = 0; i < m; ++i) tmp[i] = src[3 * i + k];
+      FVB_CUDA(cudaMemcpy(outs[k], tmp.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    *o0 = outs[0];
+    *o1 = outs[1];
+    *o2 = outs[2];
+    return FVB_OK;
+  };
+  auto up1 = [&](const auto* src, size_t m, auto** o) -> int {
+    FVB_TRY(dalloc(c, o, m));
+    FVB_CUDA(cudaMemcpy(*o, src, m * sizeof(**o), cudaMemcpyHostToDevice));
+    return FVB_OK;
+  };
+  FVB_TRY(up1(own.data(), nf, &c->own));
+  FVB_TRY(up1(nbr.data(), ni, &c->nbr));
+  FVB_TRY(up1(ptr.data(), nc + 1, &c->cf_ptr));
+  FVB_TRY(up1(cf.data(), cf.size(), &c->cf));
+  FVB_TRY(up3(sf, nf, &c->sx, &c->sy, &c->sz));
+  FVB_TRY(up1(smag, nf, &c->smag));
+  FVB_TRY(up1(vol, nc, &c->vol));
+  FVB_TRY(up1(w, ni, &c->w));
+  double *dx, *dy, *dz, *dbx, *dby, *dbz;
+  FVB_TRY(up3(d, ni, &dx, &dy, &dz));
+  FVB_TRY(up3(db, nb, &dbx, &dby, &dbz));
+  FVB_TRY(dalloc(c, &c->a, nf));
+  FVB_TRY(dalloc(c, &c->kx, nf));
+  FVB_TRY(dalloc(c, &c->ky, nf));
+  FVB_TRY(dalloc(c, &c->kz, nf));
+  FVB_TRY(op_precompute_geometry(c, dx, dy, dz, dbx, dby, dbz));
+  // coincident-centroid checks of fvm.py:349-350 / 368-370 (norms as mesh.py)
+  c->first_zero_dmag = -1;
+  for (size_t f = 0; f < ni; ++f) {
+    const double m = std::sqrt((d[3 * f] * d[3 * f] + d[3 * f + 1] * d[3 * f + 1]) +
+                               d[3 * f + 2] * d[3 * f + 2]);
+    if (m == 0.0) {
+      c->first_zero_dmag = int(f);
+      break;
+    }
+  }
+  c->dbmag_host.resize(nb);
+  for (size_t j = 0; j < nb; ++j)
+    c->dbmag_host[j] = std::sqrt((db[3 * j] * db[3 * j] + db[3 * j + 1] * db[3 * j + 1]) +
+                                 db[3 * j + 2] * db[3 * j + 2]);
+  // coupled state
+  FVB_TRY(dalloc(c, &c->u, 3 * nc));
+  FVB_TRY(dalloc(c, &c->p, nc));
+  FVB_TRY(dalloc(c, &c->flux, nf));
+  FVB_TRY(dalloc(c, &c->ub, 3 * nb));
+  FVB_TRY(dalloc(c, &c->pb, nb));
+  FVB_CUDA(cudaMemset(c->u, 0, 3 * nc * sizeof(double)));
+  FVB_CUDA(cudaMemset(c->p, 0, nc * sizeof(double)));
+  FVB_CUDA(cudaMemset(c->flux, 0, nf * sizeof(double)));
+  FVB_CUDA(cudaMemset(c->ub, 0, 3 * (nb ? nb : 1) * sizeof(double)));
+  FVB_CUDA(cudaMemset(c->pb, 0, (nb ? nb : 1) * sizeof(double)));
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  FVB_CUDA(cudaDeviceSynchronize());
+  // the temporaries dx.. stay in the allocation list (freed with the context)
+  c->have_mesh = true;
+  return FVB_OK;
+}
+
+int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
+                       const int64_t* diag_slot, const int64_t* face_addr, int64_t n_face_pairs,
+                       int64_t nnz_crs, const int64_t* crs_row_ptr, const int64_t* crs_col) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  if (c->have_pattern) {
+    fvb_set_error("pattern already uploaded");
+    return FVB_E_ARG;
+  }
+  if (c->have_mesh && n != c->nc) {
+    fvb_set_error("pattern size %lld does not match mesh cells %d", (long long)n, c->nc);
+    return FVB_E_SPARSE;
+  }
+  if (k < 1 || k > kMaxK) {
+    fvb_set_error("pattern width K=%lld outside 1..%d", (long long)k, kMaxK);
+    return FVB_E_SPARSE;
+  }
+  if (n <= 0 || n * k >= (int64_t(1) << 31)) {
+    fvb_set_error("pattern too large");
+    return FVB_E_SPARSE;
+  }
+  if (!c->have_mesh) c->nc = int(n);
+  c->k = int(k);
+  c->nnz_crs = int(nnz_crs);
+  const size_t nn = size_t(n), kk = size_t(k), nk = nn * kk;
+  std::vector<int> Is(nk), sf(nk, -1), ds(nn);
+  for (size_t i = 0; i < nn; ++i) {
+    ds[i] = int(diag_slot[i]);
+    for (size_t s = 0; s < kk; ++s) Is[s * nn + i] = int(I[i * kk + s]);
+  }
+  std::vector<int> cptr(nn + 1, 0), ccol(nnz_crs), cface(nnz_crs, -1);
+  if (nnz_crs) {
+    for (size_t i = 0; i <= nn; ++i) cptr[i] = int(crs_row_ptr[i]);
+    for (int64_t q = 0; q < nnz_crs; ++q) ccol[q] = int(crs_col[q]);
+  }
+  if (c->have_mesh && face_addr) {
+    if (n_face_pairs != c->ni) {
+      fvb_set_error("face_addr rows %lld != internal faces %d", (long long)n_face_pairs, c->ni);
+      return FVB_E_SPARSE;
+    }
+    const int64_t split = int64_t(nk);
+    for (int64_t f = 0; f < n_face_pairs; ++f) {
+      for (int side = 0; side < 2; ++side) {
+        const int64_t a = face_addr[2 * f + side];
+        int* slot;
+        if (a < split) {
+          slot = &sf[size_t(a % k) * nn + size_t(a / k)];
+        } else {
+          slot = &cface[size_t(a - split)];
+        }
+        if (*slot >= 0) {
+          fvb_set_error("faces %d and %lld join the same pair of cells; the device path "
+                        "needs one face per cell pair", *slot, (long long)f);
+          return FVB_E_SPARSE;
+        }
+        *slot = int(f);
+      }
+    }
+  }
+  auto up = [&](const std::vector<int>& v, int** o) -> int {
+    FVB_TRY(dalloc(c, o, v.size()));
+    if (!v.empty()) FVB_CUDA(cudaMemcpy(*o, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return FVB_OK;
+  };
+  FVB_TRY(up(Is, &c->I));
+  FVB_TRY(up(ds, &c->diag_slot));
+  FVB_TRY(up(sf, &c->slot_face));
+  if (nnz_crs) {
+    FVB_TRY(up(cptr, &c->crs_ptr));
+    FVB_TRY(up(ccol, &c->crs_col));
+    FVB_TRY(up(cface, &c->crs_face));
+  }
+  // solver scratch: BiCGStab x3 needs 1 + 8*3 vectors
+  c->scratch_n = 26 * nn;
+  FVB_TRY(dalloc(c, &c->scratch, c->scratch_n));
+  c->have_pattern = true;
+  return FVB_OK;
+}
+
+int fvb_set_bcs(fvb_ctx* h, int field, const uint8_t* kind, const int32_t* patch,
+                const double* fixed, int n_patches) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  if (field < 0 || field > 1) {
+    fvb_set_error("field must be 0 (u) or 1 (p)");
+    return FVB_E_ARG;
+  }
+  const int ncomp = field == 0 ? 3 : 1;
+  const size_t nb = c->nb;
+  if (!c->have_bc[field]) {
+    FVB_TRY(dalloc(c, &c->bc_kind[field], nb));
+    FVB_TRY(dalloc(c, &c->bc_patch[field], nb));
+    FVB_TRY(dalloc(c, &c->bc_fixed[field], ncomp * nb));
+    FVB_TRY(dalloc(c, &c->bc_speed[field], size_t(std::max(n_patches, 1)) + 64));
+  }
+  if (n_patches > 64 + std::max(c->n_patches[field], 1) && c->have_bc[field]) {
+    fvb_set_error("patch count changed");
+    return FVB_E_ARG;
+  }
+  c->n_patches[field] = n_patches;
+  if (nb) {
+    FVB_CUDA(cudaMemcpy(c->bc_kind[field], kind, nb, cudaMemcpyHostToDevice));
+    FVB_CUDA(cudaMemcpy(c->bc_patch[field], patch, nb * sizeof(int), cudaMemcpyHostToDevice));
+    FVB_CUDA(cudaMemcpy(c->bc_fixed[field], fixed, ncomp * nb * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  c->first_zero_dbmag_value[field] = -1;
+  for (size_t j = 0; j < nb; ++j)
+    if (bc_is_value(kind[j]) && c->dbmag_host[j] == 0.0) {
+      c->first_zero_dbmag_value[field] = int(c->ni + j);
+      break;
+    }
+  c->have_bc[field] = true;
+  return FVB_OK;
+}
+
+int fvb_set_state(fvb_ctx* h, const double* u, const double* p, const double* flux,
+                  const double* ub, const double* pb) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  if (u) FVB_TRY(h2d(c, c->u, u, 3 * size_t(c->nc)));
+  if (p) FVB_TRY(h2d(c, c->p, p, size_t(c->nc)));
+  if (flux) FVB_TRY(h2d(c, c->flux, flux, size_t(c->nf)));
+  if (ub) FVB_TRY(h2d(c, c->ub, ub, 3 * size_t(c->nb)));
+  if (pb) FVB_TRY(h2d(c, c->pb, pb, size_t(c->nb)));
+  return sync(c);
+}
+
+int fvb_get_state(fvb_ctx* h, double* u, double* p, double* flux, double* ub, double* pb) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  if (u) FVB_TRY(d2h(c, u, c->u, 3 * size_t(c->nc)));
+  if (p) FVB_TRY(d2h(c, p, c->p, size_t(c->nc)));
+  if (flux) FVB_TRY(d2h(c, flux, c->flux, size_t(c->nf)));
+  if (ub) FVB_TRY(d2h(c, ub, c->ub, 3 * size_t(c->nb)));
+  if (pb) FVB_TRY(d2h(c, pb, c->pb, size_t(c->nb)));
+  return sync(c);
+}
+
+// ----------------------------------------------------------- operators
+int fvb_op_smvp(fvb_ctx* h, const double* V, const double* crs, const double* x, double* y) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_pattern(c));
+  DevMatrix M;
+  FVB_TRY(upload_matrix(c, M, V, crs));
+  Tmp tx, ty;
+  double *dx, *dy;
+  FVB_TRY(tmp_upload(c, tx, x, c->nc, &dx));
+  FVB_TRY(tmp_zero(c, ty, c->nc, &dy));
+  FVB_TRY(smvp(c, M.m, dx, dy));
+  FVB_TRY(d2h(c, y, dy, c->nc));
+  return sync(c);
+}
+
+static int solve_common(fvb_ctx* h, bool use_cg, int ncomp, const double* V, const double* crs,
+                        const double* b, const double* x0, double* x, double tol, double abs_tol,
+                        int max_iters, fvb_solve_report* reps) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_pattern(c));
+  const size_t n = c->nc;
+  DevMatrix M;
+  FVB_TRY(upload_matrix(c, M, V, crs));
+  Tmp tb, tx;
+  double *db, *dx;
+  FVB_TRY(tmp_upload(c, tb, b, ncomp * n, &db));
+  FVB_TRY(tmp_upload(c, tx, x0, ncomp * n, &dx));
+  FVB_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  SolveOut out[3];
+  if (use_cg) {
+    FVB_TRY(cg_solve(c, M.m, db, dx, tol, abs_tol, max_iters, out));
+  } else {
+    const double* bb[3] = {db, db + n, db + 2 * n};
+    double* xx[3] = {dx, dx + n, dx + 2 * n};
+    FVB_TRY(bicgstab_solve(c, M.m, ncomp, bb, xx, tol, abs_tol, max_iters, out));
+  }
+  FVB_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  FVB_TRY(d2h(c, x, dx, ncomp * n));
+  FVB_TRY(sync(c));
+  const double wall = ev_ms(c, 0, 1) * 1e-3;
+  for (int k = 0; k < ncomp; ++k) {
+    fill_report(reps[k], out[k]);
+    reps[k].wall_time = wall;
+  }
+  for (int k = 0; k < ncomp; ++k) {
+    if (out[k].error_kind != SE_NONE) {
+      std::string msg = solve_error_text(use_cg ? "cg" : "bicgstab", out[k], out[k].error_iteration);
+      fvb_set_error("%s", msg.c_str());
+      return out[k].error_kind == SE_TIMEOUT ? FVB_E_TIMEOUT : FVB_E_SOLVER;
+    }
+  }
+  return FVB_OK;
+}
+
+int fvb_op_cg(fvb_ctx* h, const double* V, const double* crs, const double* b, const double* x0,
+              double* x, double tol, double abs_tol, int max_iters, fvb_solve_report* rep) {
+  return solve_common(h, true, 1, V, crs, b, x0, x, tol, abs_tol, max_iters, rep);
+}
+
+int fvb_op_bicgstab(fvb_ctx* h, const double* V, const double* crs, const double* b,
+                    const double* x0, double* x, double tol, double abs_tol, int max_iters,
+                    fvb_solve_report* rep) {
+  return solve_common(h, false, 1, V, crs, b, x0, x, tol, abs_tol, max_iters, rep);
+}
+
+int fvb_op_bicgstab_batched(fvb_ctx* h, int ncomp, const double* V, const double* crs,
+                            const double* b, const double* x0, double* x, double tol,
+                            double abs_tol, int max_iters, fvb_solve_report* reps) {
+  if (ncomp != 1 && ncomp != 3) {
+    fvb_set_error("ncomp must be 1 or 3");
+    return FVB_E_ARG;
+  }
+  return solve_common(h, false, ncomp, V, crs, b, x0, x, tol, abs_tol, max_iters, reps);
+}
+
+int fvb_op_apply_bcs(fvb_ctx* h, int field, const double* values, const double* speeds,
+                     double* boundary) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, field));
+  const int ncomp = field == 0 ? 3 : 1;
+  if (speeds && c->n_patches[field]) FVB_TRY(h2d(c, c->bc_speed[field], speeds, size_t(c->n_patches[field])));
+  Tmp tv, tb;
+  double *dv, *db;
+  FVB_TRY(tmp_upload(c, tv, values, ncomp * size_t(c->nc), &dv));
+  FVB_TRY(tmp_zero(c, tb, ncomp * size_t(c->nb), &db));
+  FVB_TRY(op_apply_bcs(c, field, ncomp, dv, db));
+  FVB_TRY(d2h(c, boundary, db, ncomp * size_t(c->nb)));
+  return sync(c);
+}
+
+int fvb_op_interpolate(fvb_ctx* h, int field, int ncomp, const double* values,
+                       const double* boundary, double* face_values) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  if (field >= 0) FVB_TRY(need_bc(c, field));
+  Tmp tv, tb, tf;
+  double *dv, *db = nullptr, *df;
+  FVB_TRY(tmp_upload(c, tv, values, ncomp * size_t(c->nc), &dv));
+  FVB_TRY(tmp_upload(c, tb, boundary, boundary ? ncomp * size_t(c->nb) : 0, &db));
+  FVB_TRY(tmp_zero(c, tf, ncomp * size_t(c->nf), &df));
+  FVB_TRY(op_interp(c, field, ncomp, dv, db, df));
+  FVB_TRY(d2h(c, face_values, df, ncomp * size_t(c->nf)));
+  return sync(c);
+}
+
+int fvb_op_gradient(fvb_ctx* h, int field, int ncomp, const double* values,
+                    const double* boundary, double* grad) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, field));
+  Tmp tv, tb, tg;
+  double *dv, *db, *dg;
+  FVB_TRY(tmp_upload(c, tv, values, ncomp * size_t(c->nc), &dv));
+  FVB_TRY(tmp_upload(c, tb, boundary, ncomp * size_t(c->nb), &db));
+  FVB_TRY(tmp_zero(c, tg, 3 * ncomp * size_t(c->nc), &dg));
+  FVB_TRY(op_gradient(c, field, ncomp, dv, db, dg));
+  FVB_TRY(d2h(c, grad, dg, 3 * ncomp * size_t(c->nc)));
+  return sync(c);
+}
+
+int fvb_op_divergence(fvb_ctx* h, const double* flux, double* div) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  Tmp tf, td;
+  double *df, *dd;
+  FVB_TRY(tmp_upload(c, tf, flux, size_t(c->nf), &df));
+  FVB_TRY(tmp_zero(c, td, size_t(c->nc), &dd));
+  FVB_TRY(op_divergence(c, df, dd));
+  FVB_TRY(d2h(c, div, dd, size_t(c->nc)));
+  return sync(c);
+}
+
+int fvb_op_laplacian(fvb_ctx* h, int field, int ncomp, double* V, double* crs, double* rhs,
+                     double gamma, const double* gamma_faces, const double* values,
+                     const double* boundary, int nonorth, double limiter, double coeff,
+                     double* coef, double* corr) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_pattern(c));
+  FVB_TRY(need_bc(c, field));
+  DevMatrix M;
+  FVB_TRY(upload_matrix(c, M, V, crs));
+  Tmp tr, tg, tv, tb, tgr, tco, tcr;
+  double *dr, *dg = nullptr, *dv, *db, *dgr, *dco, *dcr;
+  const size_t n = c->nc, nf = c->nf, nb = c->nb;
+  FVB_TRY(tmp_upload(c, tr, rhs, ncomp * n, &dr));
+  if (gamma_faces) FVB_TRY(tmp_upload(c, tg, gamma_faces, nf, &dg));
+  FVB_TRY(tmp_upload(c, tv, values, ncomp * n, &dv));
+  FVB_TRY(tmp_upload(c, tb, boundary, ncomp * nb, &db));
+  FVB_TRY(tmp_zero(c, tgr, 3 * ncomp * n, &dgr));
+  FVB_TRY(tmp_zero(c, tco, nf, &dco));
+  FVB_TRY(tmp_zero(c, tcr, ncomp * nf, &dcr));
+  if (nonorth && limiter > 0.0) FVB_TRY(op_gradient(c, field, ncomp, dv, db, dgr));
+  FVB_TRY(op_laplacian(c, field, ncomp, M.m, dr, gamma, dg, dv, db, dgr, nonorth, limiter, coeff,
+                       dco, dcr));
+  FVB_TRY(download_matrix(c, M, V, crs));
+  FVB_TRY(d2h(c, rhs, dr, ncomp * n));
+  if (coef) FVB_TRY(d2h(c, coef, dco, nf));
+  if (corr) FVB_TRY(d2h(c, corr, dcr, ncomp * nf));
+  return sync(c);
+}
+
+int fvb_op_laplacian_flux(fvb_ctx* h, int field, int ncomp, const double* coef,
+                          const double* corr, const double* values, const double* boundary,
+                          double* flux_out) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, field));
+  const size_t n = c->nc, nf = c->nf, nb = c->nb;
+  Tmp t1, t2, t3, t4, t5;
+  double *dco, *dcr, *dv, *db, *dout;
+  FVB_TRY(tmp_upload(c, t1, coef, nf, &dco));
+  FVB_TRY(tmp_upload(c, t2, corr, ncomp * nf, &dcr));
+  FVB_TRY(tmp_upload(c, t3, values, ncomp * n, &dv));
+  FVB_TRY(tmp_upload(c, t4, boundary, ncomp * nb, &db));
+  FVB_TRY(tmp_zero(c, t5, ncomp * nf, &dout));
+  FVB_TRY(op_lap_flux(c, field, ncomp, dco, dcr, dv, db, dout));
+  FVB_TRY(d2h(c, flux_out, dout, ncomp * nf));
+  return sync(c);
+}
+
+int fvb_op_convection(fvb_ctx* h, int field, int ncomp, double* V, double* crs, double* rhs,
+                      const double* flux, const double* boundary, int scheme, double coeff) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_pattern(c));
+  FVB_TRY(need_bc(c, field));
+  DevMatrix M;
+  FVB_TRY(upload_matrix(c, M, V, crs));
+  const size_t n = c->nc, nf = c->nf, nb = c->nb;
+  Tmp t1, t2, t3;
+  double *dr, *df, *db;
+  FVB_TRY(tmp_upload(c, t1, rhs, ncomp * n, &dr));
+  FVB_TRY(tmp_upload(c, t2, flux, nf, &df));
+  FVB_TRY(tmp_upload(c, t3, boundary, ncomp * nb, &db));
+  FVB_TRY(op_convection(c, field, ncomp, M.m, dr, df, db, scheme, coeff));
+  FVB_TRY(download_matrix(c, M, V, crs));
+  FVB_TRY(d2h(c, rhs, dr, ncomp * n));
+  return sync(c);
+}
+
+int fvb_op_ddt(fvb_ctx* h, int ncomp, double* V, double* rhs, const double* old_values, double dt,
+               double coeff) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_pattern(c));
+  if (!(dt > 0.0)) {
+    fvb_set_error("dt must be positive");
+    return FVB_E_FVM;
+  }
+  std::vector<double> zero_crs(size_t(std::max(c->nnz_crs, 1)), 0.0);
+  DevMatrix M;
+  FVB_TRY(upload_matrix(c, M, V, zero_crs.data()));
+  const size_t n = c->nc;
+  Tmp t1, t2;
+  double *dr, *dold;
+  FVB_TRY(tmp_upload(c, t1, rhs, ncomp * n, &dr));
+  FVB_TRY(tmp_upload(c, t2, old_values, ncomp * n, &dold));
+  FVB_TRY(op_ddt(c, ncomp, M.m, dr, dold, dt, coeff));
+  FVB_TRY(download_matrix(c, M, V, nullptr));
+  FVB_TRY(d2h(c, rhs, dr, ncomp * n));
+  return sync(c);
+}
+
+int fvb_state_apply_bcs(fvb_ctx* h, const double* u_speeds) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, 0));
+  FVB_TRY(need_bc(c, 1));
+  if (c->n_patches[0] && u_speeds)
+    FVB_TRY(h2d(c, c->bc_speed[0], u_speeds, size_t(c->n_patches[0])));
+  FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
+  FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
+  return sync(c);
+}
+
+int fvb_op_face_flux(fvb_ctx* h, const double* values, const double* boundary,
+                     double* flux_out) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, 0));
+  Tmp tv, tb, tf;
+  double *dv, *db, *df;
+  FVB_TRY(tmp_upload(c, tv, values, 3 * size_t(c->nc), &dv));
+  FVB_TRY(tmp_upload(c, tb, boundary, 3 * size_t(c->nb), &db));
+  FVB_TRY(tmp_zero(c, tf, size_t(c->nf), &df));
+  FVB_TRY(op_face_flux(c, 3, dv, db, 0, df));
+  FVB_TRY(d2h(c, flux_out, df, size_t(c->nf)));
+  return sync(c);
+}
+
+int fvb_plain_flux(fvb_ctx* h) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, 0));
+  FVB_TRY(op_face_flux(c, 3, c->u, c->ub, 0, c->flux));
+  return sync(c);
+}
+
+int fvb_continuity_error(fvb_ctx* h, double* out) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  double* div = c->scratch;
+  if (!div) {
+    FVB_TRY(dalloc(c, &c->scratch, size_t(c->nc)));
+    div = c->scratch;
+  }
+  FVB_TRY(op_divergence(c, c->flux, div));
+  const int blocks = 2 * c->num_sms;
+  k_absmax<<<blocks, kThreads, 0, c->stream>>>(c->nc, div, c->partials);
+  FVB_CUDA(cudaGetLastError());
+  std::vector<double> hm(blocks);
+  FVB_TRY(d2h(c, hm.data(), c->partials, size_t(blocks)));
+  FVB_TRY(sync(c));
+  double m = 0.0;
+  for (double v : hm) m = std::max(m, v);
+  *out = m;
+  return FVB_OK;
+}
+
+int fvb_piso_step(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds,
+                  fvb_step_report* rep) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  return run_step(c, cfg, u_speeds, rep, true);
+}
+
+int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds,
+                     fvb_step_report* rep) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  return run_step(c, cfg, u_speeds, rep, false);
+}
+
+int fvb_timer_start(fvb_ctx* h) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_CUDA(cudaEventRecord(c->tev[0], c->stream));
+  return FVB_OK;
+}
+
+int fvb_timer_stop(fvb_ctx* h, double* ms) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_CUDA(cudaEventRecord(c->tev[1], c->stream));
+  FVB_CUDA(cudaEventSynchronize(c->tev[1]));
+  float f = 0.f;
+  FVB_CUDA(cudaEventElapsedTime(&f, c->tev[0], c->tev[1]));
+  *ms = f;
+  return FVB_OK;
+}
+
+int fvb_sync(fvb_ctx* h) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  return sync(c);
+}
+
+}  // extern "C"

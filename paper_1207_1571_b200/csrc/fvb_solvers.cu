@@ -1,0 +1,663 @@
+// Jacobi-preconditioned CG and BiCGStab as persistent, cooperatively
+// launched kernels (linsolve.py:102-282 restated for sm_100a).
+//
+// One launch runs a whole solve: rows are strided over the co-resident
+// grid, every global sync point is one grid barrier, and the dot products
+// are deterministic (fixed per-thread order -> warp-shuffle tree -> fixed
+// block order).  Every block re-reduces the per-block partials in the same
+// order, so all blocks hold identical scalars and take identical branches:
+// the reference's stopping rules (check on entry, break right after the
+// residual test, breakdown checks) run on the device with no host round
+// trip per iteration.
+//
+// CG is fused into two passes per iteration: pass A
+// rebuilds p = z + beta p on the fly for every gathered column while it
+// forms q = A p and p.q; pass B updates x and r and forms ||r||^2 and r.z.
+#include <cmath>
+
+#include "fvb_internal.cuh"
+
+namespace fvb {
+
+namespace {
+
+constexpr int kSolverThreads = 512;
+constexpr double kResFloor = 1e-30;   // linsolve.py:20
+constexpr double kTiny = 1e-300;      // linsolve.py:21
+
+struct CgParams {
+  PatternView P;
+  const double* V;
+  const double* crs;
+  const double* inv;
+  const double* b;
+  double* x;
+  double* r;
+  double* pa;
+  double* pb;
+  double* q;
+  double tol, abs_tol;
+  int max_iters;
+  unsigned* sync;
+  double* partials;
+  double* result;  // [iters, converged, res0, res, err_kind, err_iter]
+};
+
+template <int KT>
+__global__ void __launch_bounds__(kSolverThreads) k_cg(CgParams A) {
+  __shared__ double red[32 * 4];
+  __shared__ double sc[8];
+  const PatternView& P = A.P;
+  const int n = P.n;
+  const int T = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* __restrict__ inv = A.inv;
+
+  // setup: r = b - A x0, ||b||, ||r||, r.z  (linsolve.py:106-127)
+  {
+    double acc[3] = {0.0, 0.0, 0.0};
+    const double* x = A.x;
+    for (int i = tid; i < n; i += T) {
+      auto g = [&](int col) { return x[col]; };
+      double ax = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
+      const double bi = A.b[i];
+      const double ri = bi - ax;
+      A.r[i] = ri;
+      acc[0] += bi * bi;
+      acc[1] += ri * ri;
+      acc[2] += ri * (ri * inv[i]);
+    }
+    publish_partials<3>(acc, A.partials, red);
+  }
+  if (!grid_barrier(A.sync, gridDim.x)) {
+    if (tid == 0) A.result[4] = SE_TIMEOUT;
+    return;
+  }
+  double s3[3];
+  grid_sum<3>(A.partials, gridDim.x, s3, sc);
+  const double bnorm = fmax(sqrt(s3[0]), kResFloor);
+  double res = sqrt(s3[1]) / bnorm;
+  const double res0 = res;
+  double rz = s3[2];
+  int it = 0;
+  bool conv = res <= A.tol || res * bnorm <= A.abs_tol;
+  int err = SE_NONE;
+  double beta = 0.0;
+  double* pold = A.pa;
+  double* pnew = A.pb;
+  bool first = true;
+  while (!conv && it < A.max_iters) {
+    ++it;
+    // pass A: p <- z + beta p (gathered columns), q = A p, p.q
+    {
+      double acc[1] = {0.0};
+      const double* r = A.r;
+      const double* po = pold;
+      for (int i = tid; i < n; i += T) {
+        auto g = [&](int col) {
+          const double z = r[col] * inv[col];
+          return first ? z : po[col] * beta + z;
+        };
+        const double qi = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
+        const double pi = g(i);
+        pnew[i] = pi;
+        A.q[i] = qi;
+        acc[0] += pi * qi;
+      }
+      publish_partials<1>(acc, A.partials, red);
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { err = SE_TIMEOUT; break; }
+    double pq[1];
+    grid_sum<1>(A.partials, gridDim.x, pq, sc);
+    if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
+    const double alpha = rz / pq[0];
+    // pass B: x += alpha p, r -= alpha q, ||r||^2, r.z
+    {
+      double acc[2] = {0.0, 0.0};
+      for (int i = tid; i < n; i += T) {
+        const double pi = pnew[i];
+        A.x[i] = A.x[i] + alpha * pi;
+        const double ri = A.r[i] - alpha * A.q[i];
+        A.r[i] = ri;
+        acc[0] += ri * ri;
+        acc[1] += ri * (ri * inv[i]);
+      }
+      publish_partials<2>(acc, A.partials, red);
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { err = SE_TIMEOUT; break; }
+    double s2[2];
+    grid_sum<2>(A.partials, gridDim.x, s2, sc);
+    res = sqrt(s2[0]) / bnorm;
+    if (!isfinite(res)) { err = SE_DIVERGED; break; }
+    if (res <= A.tol || res * bnorm <= A.abs_tol) { conv = true; break; }
+    beta = s2[1] / rz;
+    rz = s2[1];
+    double* t = pold; pold = pnew; pnew = t;
+    first = false;
+  }
+  if (tid == 0) {
+    A.result[0] = it;
+    A.result[1] = conv ? 1.0 : 0.0;
+    A.result[2] = res0;
+    A.result[3] = res;
+    A.result[4] = err;
+    A.result[5] = err ? it : 0;
+  }
+}
+
+// ------------------------------------------------------------ BiCGStab
+template <int NC>
+struct BiParams {
+  PatternView P;
+  const double* V;
+  const double* crs;
+  const double* inv;
+  const double* b[NC];
+  double* x[NC];
+  double* r[NC];
+  double* rh[NC];
+  double* p[NC];
+  double* ph[NC];
+  double* v[NC];
+  double* s[NC];
+  double* sh[NC];
+  double* t[NC];
+  double tol, abs_tol;
+  int max_iters;
+  unsigned* sync;
+  double* partials;
+  double* result;  // per comp: [iters, converged, res0, res, err_kind, err_iter]
+};
+
+// y_c = A x_c for NC vectors sharing one pass over V and I.
+template <int KT, int NC, typename G>
+__device__ __forceinline__ void ell_rows_multi(const PatternView& P, const double* __restrict__ V,
+                                               const double* crs, int i, const bool* act,
+                                               G gather, double* y) {
+  const int n = P.n, K = KT > 0 ? KT : P.k;
+  double ev[NC], od[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) ev[c] = od[c] = 0.0;
+#pragma unroll
+  for (int s = 0; s < (KT > 0 ? KT : kMaxK); s += 2) {
+    if (KT == 0 && s >= K) break;
+    int col = __ldg(P.I + size_t(s) * n + i);
+    col = col < 0 ? 0 : col;
+    const double v = __ldg(V + size_t(s) * n + i);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (act[c]) {
+        const double pr = v * gather(c, col);
+        ev[c] = s == 0 ? pr : ev[c] + pr;
+      }
+  }
+#pragma unroll
+  for (int s = 1; s < (KT > 0 ? KT : kMaxK); s += 2) {
+    if (KT == 0 && s >= K) break;
+    int col = __ldg(P.I + size_t(s) * n + i);
+    col = col < 0 ? 0 : col;
+    const double v = __ldg(V + size_t(s) * n + i);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (act[c]) {
+        const double pr = v * gather(c, col);
+        od[c] = s == 1 ? pr : od[c] + pr;
+      }
+  }
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    if (!act[c]) continue;
+    double yy = K > 1 ? ev[c] + od[c] : ev[c];
+    if (P.nnz_crs) {
+      double tl = 0.0;
+      for (int q = P.crs_ptr[i]; q < P.crs_ptr[i + 1]; ++q) tl += crs[q] * gather(c, P.crs_col[q]);
+      yy = yy + tl;
+    }
+    y[c] = yy;
+  }
+}
+
+struct CompState {
+  int it, done, err, err_it, sconv, restart, copy, live;
+  double bn, res0, res, rho, alpha, omega, beta, rr, rhr;
+};
+
+template <int KT, int NC>
+__global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
+  __shared__ double red[32 * 2 * NC];
+  __shared__ double sc[2 * NC];
+  __shared__ CompState S[NC];
+  const PatternView& P = A.P;
+  const int n = P.n;
+  const int T = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* __restrict__ inv = A.inv;
+  bool act[NC];
+  bool timeout = false;
+
+  // setup (linsolve.py:180-196)
+  {
+    double acc[2 * NC];
+#pragma unroll
+    for (int m = 0; m < 2 * NC; ++m) acc[m] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) act[c] = true;
+    for (int i = tid; i < n; i += T) {
+      double ax[NC];
+      auto g = [&](int c, int col) { return A.x[c][col]; };
+      ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, ax);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double bi = A.b[c][i];
+        const double ri = bi - ax[c];
+        A.r[c][i] = ri;
+        A.rh[c][i] = ri;
+        acc[2 * c] += bi * bi;
+        acc[2 * c + 1] += ri * ri;
+      }
+    }
+    publish_partials<2 * NC>(acc, A.partials, red);
+  }
+  if (!grid_barrier(A.sync, gridDim.x)) {
+    if (tid == 0)
+      for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
+    return;
+  }
+  double sums[2 * NC];
+  grid_sum<2 * NC>(A.partials, gridDim.x, sums, sc);
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < NC; ++c) {
+      CompState& s = S[c];
+      s.it = 0; s.err = SE_NONE; s.err_it = 0; s.sconv = 0; s.restart = 0; s.copy = 0; s.live = 0;
+      s.bn = fmax(sqrt(sums[2 * c]), kResFloor);
+      s.res = sqrt(sums[2 * c + 1]) / s.bn;
+      s.res0 = s.res;
+      s.rr = sums[2 * c + 1];
+      s.rhr = s.rr;
+      s.done = s.res <= A.tol || s.res * s.bn <= A.abs_tol;
+      s.rho = s.alpha = s.omega = 1.0;
+      s.beta = 0.0;
+    }
+  }
+  __syncthreads();
+
+  while (!timeout) {
+    // per-component scalar logic (linsolve.py:198-219), identical in every block
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < NC; ++c) {
+        CompState& s = S[c];
+        s.sconv = 0;
+        s.live = 0;
+        if (s.done || s.err || s.it >= A.max_iters) continue;
+        s.it++;
+        double rho_new = s.it == 1 ? s.rr : s.rhr;
+        s.restart = fabs(rho_new) < kTiny;
+        if (s.restart) {
+          rho_new = s.rr;  // r_hat := r, so r_hat.r = ||r||^2
+          if (rho_new < kTiny) { s.err = SE_RHO; s.err_it = s.it; continue; }
+        }
+        s.copy = (s.it == 1 || s.restart);
+        if (!s.copy) s.beta = (rho_new / s.rho) * (s.alpha / s.omega);
+        s.rho = rho_new;
+        s.live = 1;
+      }
+    }
+    __syncthreads();
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      act[c] = S[c].live != 0;
+      any = any || act[c];
+    }
+    if (!any) break;
+    // pass P: p = r | p = (p - omega v) beta + r ; p_hat = p / D ; restart r_hat
+    for (int i = tid; i < n; i += T) {
+      const double iv = inv[i];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (!act[c]) continue;
+        const double ri = A.r[c][i];
+        double pi;
+        if (S[c].copy) {
+          pi = ri;
+        } else {
+          pi = A.p[c][i] - S[c].omega * A.v[c][i];
+          pi = pi * S[c].beta;
+          pi = pi + ri;
+        }
+        A.p[c][i] = pi;
+        A.ph[c][i] = pi * iv;
+        if (S[c].restart) A.rh[c][i] = ri;
+      }
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
+    // pass V: v = A p_hat, r_hat.v
+    {
+      double acc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+      for (int i = tid; i < n; i += T) {
+        double y[NC];
+        auto g = [&](int c, int col) { return A.ph[c][col]; };
+        ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          A.v[c][i] = y[c];
+          acc[c] += A.rh[c][i] * y[c];
+        }
+      }
+      publish_partials<NC>(acc, A.partials, red);
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
+    {
+      double rv[NC];
+      grid_sum<NC>(A.partials, gridDim.x, rv, sc);
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          if (fabs(rv[c]) < kTiny) { S[c].err = SE_RV; S[c].err_it = S[c].it; continue; }
+          S[c].alpha = S[c].rho / rv[c];
+        }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < NC; ++c) act[c] = act[c] && !S[c].err;
+    }
+    // pass S: s = r - alpha v, s_hat = s / D, ||s||^2
+    {
+      double acc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+      for (int i = tid; i < n; i += T) {
+        const double iv = inv[i];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          const double si = A.r[c][i] - S[c].alpha * A.v[c][i];
+          A.s[c][i] = si;
+          A.sh[c][i] = si * iv;
+          acc[c] += si * si;
+        }
+      }
+      publish_partials<NC>(acc, A.partials, red);
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
+    {
+      double ss[NC];
+      grid_sum<NC>(A.partials, gridDim.x, ss, sc);
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          const double sn = sqrt(ss[c]);
+          if (sn / S[c].bn <= A.tol || sn <= A.abs_tol) {
+            S[c].sconv = 1;
+            S[c].res = sn / S[c].bn;
+          }
+        }
+      __syncthreads();
+    }
+    // pass T: converged-at-s components take x += alpha p_hat; others t = A s_hat
+    bool tact[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) tact[c] = act[c] && !S[c].sconv;
+    {
+      double acc[2 * NC];
+#pragma unroll
+      for (int m = 0; m < 2 * NC; ++m) acc[m] = 0.0;
+      for (int i = tid; i < n; i += T) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          if (act[c] && S[c].sconv) A.x[c][i] = A.x[c][i] + S[c].alpha * A.ph[c][i];
+        double y[NC];
+        auto g = [&](int c, int col) { return A.sh[c][col]; };
+        ell_rows_multi<KT, NC>(P, A.V, A.crs, i, tact, g, y);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!tact[c]) continue;
+          A.t[c][i] = y[c];
+          acc[2 * c] += y[c] * y[c];
+          acc[2 * c + 1] += y[c] * A.s[c][i];
+        }
+      }
+      publish_partials<2 * NC>(acc, A.partials, red);
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
+    {
+      double tts[2 * NC];
+      grid_sum<2 * NC>(A.partials, gridDim.x, tts, sc);
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          if (S[c].sconv) { S[c].done = 1; continue; }
+          const double tt = tts[2 * c], ts = tts[2 * c + 1];
+          if (tt == 0.0) { S[c].err = SE_OMEGA; S[c].err_it = S[c].it; continue; }
+          S[c].omega = ts / tt;
+          if (fabs(S[c].omega) < kTiny) { S[c].err = SE_OMEGA; S[c].err_it = S[c].it; }
+        }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < NC; ++c) tact[c] = tact[c] && !S[c].err;
+    }
+    // pass X: x += alpha p_hat; x += omega s_hat; r = s - omega t; ||r||^2, r_hat.r
+    {
+      double acc[2 * NC];
+#pragma unroll
+      for (int m = 0; m < 2 * NC; ++m) acc[m] = 0.0;
+      for (int i = tid; i < n; i += T) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!tact[c]) continue;
+          double xi = A.x[c][i] + S[c].alpha * A.ph[c][i];
+          xi = xi + S[c].omega * A.sh[c][i];
+          A.x[c][i] = xi;
+          const double ri = A.s[c][i] - S[c].omega * A.t[c][i];
+          A.r[c][i] = ri;
+          acc[2 * c] += ri * ri;
+          acc[2 * c + 1] += A.rh[c][i] * ri;
+        }
+      }
+      publish_partials<2 * NC>(acc, A.partials, red);
+    }
+    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
+    {
+      double rr[2 * NC];
+      grid_sum<2 * NC>(A.partials, gridDim.x, rr, sc);
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!tact[c]) continue;
+          S[c].rr = rr[2 * c];
+          S[c].rhr = rr[2 * c + 1];
+          S[c].res = sqrt(rr[2 * c]) / S[c].bn;
+          if (!isfinite(S[c].res)) { S[c].err = SE_DIVERGED; S[c].err_it = S[c].it; continue; }
+          if (S[c].res <= A.tol || S[c].res * S[c].bn <= A.abs_tol) S[c].done = 1;
+        }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    for (int c = 0; c < NC; ++c) {
+      A.result[6 * c + 0] = S[c].it;
+      A.result[6 * c + 1] = S[c].done ? 1.0 : 0.0;
+      A.result[6 * c + 2] = S[c].res0;
+      A.result[6 * c + 3] = S[c].res;
+      A.result[6 * c + 4] = timeout ? SE_TIMEOUT : S[c].err;
+      A.result[6 * c + 5] = S[c].err_it;
+    }
+  }
+}
+
+template <typename K>
+int coop_blocks(Ctx* c, K kernel, int* blocks) {
+  int per_sm = 0;
+  FVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSolverThreads, 0));
+  if (per_sm < 1) {
+    fvb_set_error("solver kernel cannot be resident");
+    return FVB_E_CUDA;
+  }
+  if (per_sm > 2) per_sm = 2;
+  *blocks = per_sm * c->num_sms;
+  return FVB_OK;
+}
+
+template <typename K, typename Args>
+int coop_launch(Ctx* c, K kernel, Args& args) {
+  int blocks = 0;
+  FVB_TRY(coop_blocks(c, kernel, &blocks));
+  FVB_CUDA(cudaMemsetAsync(c->sync, 0, 4 * sizeof(unsigned), c->stream));
+  void* params[] = {&args};
+  FVB_CUDA(cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads),
+                                       params, 0, c->stream));
+  return FVB_OK;
+}
+
+int check_zero_diag(Ctx* c, MatView A, double* inv, int* zero_row) {
+  int* dz = c->ipart;
+  const int big = 0x7fffffff;
+  FVB_CUDA(cudaMemcpyAsync(dz, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  FVB_TRY(launch_inv_diag(c, A.V, inv, dz));
+  FVB_CUDA(cudaMemcpyAsync(zero_row, dz, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  return FVB_OK;
+}
+
+}  // namespace
+
+std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row) {
+  char buf[256];
+  switch (o.error_kind) {
+    case SE_ZERO_DIAG:
+      snprintf(buf, sizeof buf, "singular preconditioner: zero diagonal at row %d", zero_row);
+      break;
+    case SE_CG_NOT_SPD:
+      snprintf(buf, sizeof buf, "cg: matrix not positive definite at iteration %d", o.error_iteration);
+      break;
+    case SE_DIVERGED:
+      snprintf(buf, sizeof buf, "%s: residual diverged at iteration %d", solver, o.error_iteration);
+      break;
+    case SE_RHO:
+      snprintf(buf, sizeof buf, "bicgstab: rho breakdown at iteration %d", o.error_iteration);
+      break;
+    case SE_RV:
+      snprintf(buf, sizeof buf, "bicgstab: breakdown (r_hat . v = 0) at iteration %d",
+               o.error_iteration);
+      break;
+    case SE_OMEGA:
+      snprintf(buf, sizeof buf, "bicgstab: omega breakdown at iteration %d", o.error_iteration);
+      break;
+    case SE_TIMEOUT:
+      snprintf(buf, sizeof buf, "%s: device watchdog fired (grid barrier timeout)", solver);
+      break;
+    default:
+      snprintf(buf, sizeof buf, "%s: ok", solver);
+  }
+  return buf;
+}
+
+// Work buffers live in the context scratch pool: layout per call.
+int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double abs_tol,
+             int max_iters, SolveOut* out) {
+  const size_t n = c->nc;
+  double* inv = c->scratch;
+  double* r = inv + n;
+  double* pa = r + n;
+  double* pb = pa + n;
+  double* q = pb + n;
+  double* result = c->partials + 16 * 4096;
+  int zero_row = 0x7fffffff;
+  FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
+  *out = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0};
+  if (zero_row != 0x7fffffff) {
+    out->error_kind = SE_ZERO_DIAG;
+    out->error_iteration = zero_row;
+    return FVB_OK;
+  }
+  CgParams prm{c->pattern(), A.V, A.crs, inv, b, x, r, pa, pb, q, tol, abs_tol, max_iters,
+               c->sync, c->partials, result};
+  switch (c->k) {
+    case 5: FVB_TRY(coop_launch(c, k_cg<5>, prm)); break;
+    case 7: FVB_TRY(coop_launch(c, k_cg<7>, prm)); break;
+    default: FVB_TRY(coop_launch(c, k_cg<0>, prm)); break;
+  }
+  double h[6];
+  FVB_CUDA(cudaMemcpyAsync(h, result, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  out->iterations = int(h[0]);
+  out->converged = int(h[1]);
+  out->res0 = h[2];
+  out->res = h[3];
+  out->error_kind = int(h[4]);
+  out->error_iteration = int(h[5]);
+  return FVB_OK;
+}
+
+template <int NC>
+static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const* x, double tol,
+                       double abs_tol, int max_iters, double* inv, double* result) {
+  const size_t n = c->nc;
+  BiParams<NC> prm;
+  prm.P = c->pattern();
+  prm.V = A.V;
+  prm.crs = A.crs;
+  prm.inv = inv;
+  double* w = inv + n;
+  for (int k = 0; k < NC; ++k) {
+    prm.b[k] = b[k];
+    prm.x[k] = x[k];
+    prm.r[k] = w; w += n;
+    prm.rh[k] = w; w += n;
+    prm.p[k] = w; w += n;
+    prm.ph[k] = w; w += n;
+    prm.v[k] = w; w += n;
+    prm.s[k] = w; w += n;
+    prm.sh[k] = w; w += n;
+    prm.t[k] = w; w += n;
+  }
+  prm.tol = tol;
+  prm.abs_tol = abs_tol;
+  prm.max_iters = max_iters;
+  prm.sync = c->sync;
+  prm.partials = c->partials;
+  prm.result = result;
+  switch (c->k) {
+    case 5: return coop_launch(c, k_bicgstab<5, NC>, prm);
+    case 7: return coop_launch(c, k_bicgstab<7, NC>, prm);
+    default: return coop_launch(c, k_bicgstab<0, NC>, prm);
+  }
+}
+
+int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double* const* x,
+                   double tol, double abs_tol, int max_iters, SolveOut* out) {
+  double* inv = c->scratch;
+  double* result = c->partials + 16 * 4096;
+  int zero_row = 0x7fffffff;
+  FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
+  for (int k = 0; k < ncomp; ++k) out[k] = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0};
+  if (zero_row != 0x7fffffff) {
+    out[0].error_kind = SE_ZERO_DIAG;
+    out[0].error_iteration = zero_row;
+    return FVB_OK;
+  }
+  if (ncomp == 1)
+    FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  else if (ncomp == 3)
+    FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  else {
+    fvb_set_error("bicgstab batch supports 1 or 3 components");
+    return FVB_E_ARG;
+  }
+  double h[18];
+  FVB_CUDA(cudaMemcpyAsync(h, result, sizeof(double) * 6 * ncomp, cudaMemcpyDeviceToHost,
+                           c->stream));
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < ncomp; ++k) {
+    out[k].iterations = int(h[6 * k]);
+    out[k].converged = int(h[6 * k + 1]);
+    out[k].res0 = h[6 * k + 2];
+    out[k].res = h[6 * k + 3];
+    out[k].error_kind = int(h[6 * k + 4]);
+    out[k].error_iteration = int(h[6 * k + 5]);
+  }
+  return FVB_OK;
+}
+
+}  // namespace fvb

@@ -1,0 +1,221 @@
+"""Face-addressed polyhedral mesh and its geometry (reference: mesh.py).
+
+Same data model as the reference: owner/neighbour face addressing,
+internal faces first with owner < neighbour, boundary faces grouped in
+contiguous patches.  ``compute_geometry`` runs the native builder in
+libfvb (fvb_geometry), which replays the reference's numpy arithmetic
+operation by operation, so every metric array is bit-identical to
+fvflow.mesh.compute_geometry (mesh.py:173-278).
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import MeshError
+
+PATCH_KINDS = ("wall", "inlet", "outlet", "empty")
+MAX_NONORTHOGONALITY_DEG = 80.0  # mesh.py:24
+
+__all__ = [
+    "PATCH_KINDS", "MAX_NONORTHOGONALITY_DEG", "MeshError", "Patch", "Mesh",
+    "MeshGeometry", "compute_geometry", "cell_face_adjacency", "cell_neighbour_counts",
+    "max_neighbours", "closedness_error",
+]
+
+
+@dataclass
+class Patch:
+    """Contiguous run of boundary faces sharing a physical role (mesh.py:30-42)."""
+
+    name: str
+    kind: str
+    start: int
+    count: int
+
+    @property
+    def faces(self):
+        return np.arange(self.start, self.start + self.count)
+
+
+@dataclass
+class Mesh:
+    """Polyhedral mesh in owner/neighbour face addressing (mesh.py:45-128)."""
+
+    points: np.ndarray
+    face_points: np.ndarray
+    face_offsets: np.ndarray
+    owner: np.ndarray
+    neighbour: np.ndarray
+    patches: list = field(default_factory=list)
+    n_cells: int = 0
+
+    @property
+    def n_faces(self):
+        return len(self.owner)
+
+    @property
+    def n_internal(self):
+        return len(self.neighbour)
+
+    @property
+    def n_boundary(self):
+        return self.n_faces - self.n_internal
+
+    @property
+    def n_points(self):
+        return len(self.points)
+
+    def patch_by_name(self, name):
+        for p in self.patches:
+            if p.name == name:
+                return p
+        raise KeyError(f"no patch named {name!r}")
+
+    def face_patch_ids(self):
+        ids = np.full(self.n_faces, -1, dtype=np.int64)
+        for i, p in enumerate(self.patches):
+            ids[p.start:p.start + p.count] = i
+        return ids
+
+    def validate(self):
+        """Structural invariants; MeshError on the first failure (mesh.py:90-128)."""
+        nf, ni, nc = self.n_faces, self.n_internal, self.n_cells
+        off = np.asarray(self.face_offsets)
+        if len(off) != nf + 1:
+            raise MeshError("face_offsets length does not match face count")
+        counts = np.diff(off)
+        if counts.min(initial=3) < 3:
+            raise MeshError(f"face {int(np.argmax(counts < 3))} has fewer than 3 points")
+        fp = np.asarray(self.face_points)
+        if fp.min(initial=0) < 0 or (nf and fp.max() >= self.n_points):
+            raise MeshError("face point index out of range")
+        own = np.asarray(self.owner)
+        if own.min(initial=0) < 0 or (nf and own.max() >= nc):
+            raise MeshError("owner cell index out of range")
+        if ni:
+            nbr = np.asarray(self.neighbour)
+            if nbr.min() < 0 or nbr.max() >= nc:
+                raise MeshError("neighbour cell index out of range")
+            bad = ~(own[:ni] < nbr)
+            if bad.any():
+                raise MeshError(f"internal face {int(np.argmax(bad))}: owner must be < neighbour")
+        covered = np.zeros(nf - ni, dtype=bool)
+        for p in self.patches:
+            if p.kind not in PATCH_KINDS:
+                raise MeshError(f"patch {p.name!r} has unknown kind {p.kind!r}")
+            if p.start < ni or p.start + p.count > nf:
+                raise MeshError(f"patch {p.name!r} extends outside boundary faces")
+            seg = covered[p.start - ni:p.start - ni + p.count]
+            if seg.any():
+                raise MeshError(f"patch {p.name!r} overlaps another patch")
+            seg[:] = True
+        if not covered.all():
+            raise MeshError("boundary faces not fully covered by patches")
+        touched = np.zeros(nc, dtype=bool)
+        touched[own] = True
+        touched[np.asarray(self.neighbour)] = True
+        if not touched.all():
+            raise MeshError(f"cell {int(np.argmax(~touched))} has no faces")
+
+
+@dataclass
+class MeshGeometry:
+    """Metric quantities per face or cell (mesh.py:131-151)."""
+
+    cell_volume: np.ndarray
+    cell_centroid: np.ndarray
+    face_area: np.ndarray
+    face_area_mag: np.ndarray
+    face_centroid: np.ndarray
+    d: np.ndarray
+    d_mag: np.ndarray
+    weight: np.ndarray
+    nonorth_deg: np.ndarray
+    d_boundary: np.ndarray
+    d_boundary_mag: np.ndarray
+
+    @property
+    def max_nonorth_deg(self):
+        return float(self.nonorth_deg.max()) if len(self.nonorth_deg) else 0.0
+
+
+def compute_geometry(mesh, check=True) -> MeshGeometry:
+    """Native fan-triangle / tet-decomposition metrics (fvb_geometry).
+
+    Raises MeshError for zero-area faces, non-positive volumes, inverted
+    internal faces and (check=True) faces beyond 80 deg non-orthogonality.
+    """
+    nf, ni, nc = mesh.n_faces, mesh.n_internal, mesh.n_cells
+    nb = nf - ni
+    pts = _lib.f64(mesh.points)
+    off = _lib.i64(mesh.face_offsets)
+    fp = _lib.i64(mesh.face_points)
+    own = _lib.i64(mesh.owner)
+    nbr = _lib.i64(mesh.neighbour)
+    vol = np.empty(nc)
+    cc = np.empty((nc, 3))
+    sf = np.empty((nf, 3))
+    smag = np.empty(nf)
+    fc = np.empty((nf, 3))
+    d = np.empty((ni, 3))
+    dmag = np.empty(ni)
+    w = np.empty(ni)
+    cosang = np.empty(ni)
+    db = np.empty((nb, 3))
+    dbmag = np.empty(nb)
+    P = _lib.ptr
+    rc = _lib.lib.fvb_geometry(
+        len(pts), P(pts), nf, P(off, _lib.i64p), P(fp, _lib.i64p), nc, ni,
+        P(own, _lib.i64p), P(nbr, _lib.i64p), int(bool(check)), P(vol), P(cc), P(sf),
+        P(smag), P(fc), P(d), P(dmag), P(w), P(cosang), P(db), P(dbmag))
+    _lib.check(rc, MeshError)
+    # numpy's own arccos/degrees for the reported angle (mesh.py:254-255)
+    nonorth = np.degrees(np.arccos(cosang))
+    if check and ni and nonorth.max() > MAX_NONORTHOGONALITY_DEG:
+        bad = int(np.argmax(nonorth))
+        raise MeshError(
+            f"internal face {bad} is {nonorth[bad]:.1f} deg non-orthogonal "
+            f"(limit {MAX_NONORTHOGONALITY_DEG:g})"
+        )
+    return MeshGeometry(cell_volume=vol, cell_centroid=cc, face_area=sf, face_area_mag=smag,
+                        face_centroid=fc, d=d, d_mag=dmag, weight=w, nonorth_deg=nonorth,
+                        d_boundary=db, d_boundary_mag=dbmag)
+
+
+def cell_face_adjacency(mesh):
+    """Per-cell (face, sign, other) triples (mesh.py:281-300); host utility."""
+    ni = mesh.n_internal
+    pid = mesh.face_patch_ids()
+    adj = [[] for _ in range(mesh.n_cells)]
+    own, nbr = mesh.owner, mesh.neighbour
+    for f in range(mesh.n_faces):
+        o = int(own[f])
+        if f < ni:
+            n = int(nbr[f])
+            adj[o].append((f, 1, n))
+            adj[n].append((f, -1, o))
+        else:
+            adj[o].append((f, 1, -(int(pid[f]) + 1)))
+    return adj
+
+
+def cell_neighbour_counts(mesh):
+    ni = mesh.n_internal
+    return (np.bincount(mesh.owner[:ni], minlength=mesh.n_cells)
+            + np.bincount(mesh.neighbour, minlength=mesh.n_cells))
+
+
+def max_neighbours(mesh):
+    c = cell_neighbour_counts(mesh)
+    return int(c.max()) if len(c) else 0
+
+
+def closedness_error(mesh, geom):
+    """Max over cells of |sum of outward area vectors| (mesh.py:317-327)."""
+    ni = mesh.n_internal
+    acc = np.zeros((mesh.n_cells, 3))
+    np.add.at(acc, mesh.owner, geom.face_area)
+    np.add.at(acc, mesh.neighbour, -geom.face_area[:ni])
+    return float(np.linalg.norm(acc, axis=1).max())

@@ -1,0 +1,123 @@
+"""Device CG / BiCGStab against the reference's solver semantics
+(linsolve.py:102-282): golden solves, dense oracles, error contract."""
+
+import numpy as np
+import pytest
+
+from golden_io import CASES, golden_case, rel
+from paper_1207_1571_b200 import fvm, linsolve, mesh as pmesh, sparse
+from paper_1207_1571_b200.errors import SolverError
+from paper_1207_1571_b200.linsolve import SolveConfig, bicgstab, bicgstab_batched, cg
+
+pytestmark = pytest.mark.gpu
+
+
+def hybrid_from_dense(dense):
+    n = len(dense)
+    struct = (dense != 0) | (dense.T != 0)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n) if struct[i, j]]
+    p = sparse.pattern_from_pairs(n, pairs, n)
+    A = sparse.HybridMatrix.zeros(p)
+    for i in range(n):
+        for j in range(n):
+            if i == j or struct[i, j]:
+                sparse.coeff_accumulate(A, p.address(i, j), dense[i, j], add=False)
+    return A
+
+
+def random_spd(rng, n):
+    dense = np.zeros((n, n))
+    iu, ju = np.triu_indices(n, 1)
+    mask = rng.random(len(iu)) < 0.2
+    dense[iu[mask], ju[mask]] = rng.normal(size=mask.sum())
+    dense += dense.T
+    dense[np.diag_indices(n)] = np.abs(dense).sum(axis=1) + rng.uniform(0.5, 2.0, n)
+    return dense
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_golden_solves(name):
+    case, g = golden_case(name)
+    pat = sparse.build_pattern(case.mesh)
+    n = case.mesh.n_cells
+    A = sparse.HybridMatrix.zeros(pat)
+    A.V[:] = g["sol_cg_V"]
+    x, rep = cg(A, g["in_b"], np.zeros(n), SolveConfig(tolerance=1e-10, max_iters=5000))
+    ref = g["sol_cg_rep"]
+    assert rep.converged and abs(rep.iterations - ref[0]) <= 1
+    assert abs(rep.initial_residual - ref[1]) <= 1e-12 * ref[1]
+    assert rel(x, g["sol_cg_x"]) < 1e-8
+    M = sparse.HybridMatrix.zeros(pat)
+    M.V[:] = g["op_lapv_V"]
+    x, rep = bicgstab(M, g["in_b"], np.zeros(n), SolveConfig(tolerance=1e-10, max_iters=5000))
+    ref = g["sol_bi_rep"]
+    assert rep.converged and abs(rep.iterations - ref[0]) <= 2
+    assert rel(x, g["sol_bi_x"]) < 1e-8
+
+
+def test_cg_identity_and_2x2():
+    p = sparse.pattern_from_pairs(6, [], 1)
+    A = sparse.HybridMatrix.zeros(p)
+    A.V[:, 0] = 1.0
+    b = np.arange(1.0, 7.0)
+    x, rep = cg(A, b, np.zeros(6), SolveConfig(tolerance=1e-12))
+    assert np.allclose(x, b, atol=1e-14) and rep.iterations <= 1 and rep.converged
+    A = hybrid_from_dense(np.array([[4.0, 1.0], [1.0, 3.0]]))
+    x0 = np.array([0.3, 0.4])
+    keep = x0.copy()
+    x, rep = cg(A, np.array([1.0, 2.0]), x0, SolveConfig(tolerance=1e-13))
+    assert np.allclose(x, [1 / 11, 7 / 11], atol=1e-10) and rep.iterations <= 2
+    assert (x0 == keep).all()
+
+
+def test_cg_random_spd_vs_dense():
+    rng = np.random.default_rng(77)
+    for _ in range(30):
+        n = int(rng.integers(2, 51))
+        dense = random_spd(rng, n)
+        A = hybrid_from_dense(dense)
+        b = rng.normal(size=n)
+        x, rep = cg(A, b, np.zeros(n), SolveConfig(tolerance=1e-11, max_iters=2 * n))
+        assert rep.converged and rep.iterations <= 2 * n
+        assert np.allclose(x, np.linalg.solve(dense, b), rtol=1e-8, atol=1e-9)
+
+
+def test_bicgstab_nonsymmetric_vs_dense_and_batched():
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        n = int(rng.integers(3, 40))
+        dense = random_spd(rng, n)
+        dense += np.triu(rng.normal(scale=0.3, size=(n, n)) * (dense != 0), 1)
+        A = hybrid_from_dense(dense)
+        B = rng.normal(size=(n, 3))
+        cfg = SolveConfig(tolerance=1e-11, max_iters=500)
+        xs = []
+        for c in range(3):
+            x, rep = bicgstab(A, B[:, c], np.zeros(n), cfg)
+            assert rep.converged
+            assert np.allclose(x, np.linalg.solve(dense, B[:, c]), rtol=1e-7, atol=1e-9)
+            xs.append((x, rep))
+        X, reps = bicgstab_batched(A, B, np.zeros((n, 3)), cfg)
+        for c in range(3):
+            assert np.array_equal(X[:, c], xs[c][0])
+            assert reps[c].iterations == xs[c][1].iterations
+
+
+def test_error_contract():
+    A = hybrid_from_dense(np.array([[0.0, 1.0], [1.0, 3.0]]))
+    with pytest.raises(SolverError, match="row 0"):
+        cg(A, np.ones(2), np.zeros(2), SolveConfig())
+    A = hybrid_from_dense(np.array([[-1.0, 0.0], [0.0, -2.0]]))
+    with pytest.raises(SolverError, match="not positive definite at iteration 1"):
+        cg(A, np.ones(2), np.zeros(2), SolveConfig())
+    dense = np.array([[4.0, 1.0], [1.0, 3.0]])
+    A = hybrid_from_dense(dense)
+    x, rep = cg(A, np.zeros(2), np.zeros(2), SolveConfig())
+    assert rep.iterations == 0 and rep.converged and rep.initial_residual == 0.0
+    x, rep = cg(random_spd_hybrid(40), np.ones(40), np.zeros(40),
+                SolveConfig(tolerance=1e-30, max_iters=3))
+    assert rep.iterations == 3 and not rep.converged
+
+
+def random_spd_hybrid(n):
+    return hybrid_from_dense(random_spd(np.random.default_rng(1), n))
