@@ -227,6 +227,11 @@ int fvb_op_face_flux(fvb_ctx* ctx, const double* values, const double* boundary,
 int fvb_plain_flux(fvb_ctx* ctx);
 /* continuity_error (coupling.py:373-375) */
 int fvb_continuity_error(fvb_ctx* ctx, double* out);
+/* number of kernels libfvb has launched in this process (bench evidence) */
+unsigned long long fvb_launch_count(void);
+/* page-lock caller-owned host buffers (pinned H2D/D2H for the e2e path) */
+int fvb_host_register(void* ptr, int64_t bytes);
+int fvb_host_unregister(void* ptr);
 /* device timer on the context stream (CUDA events): start, then stop
  * (synchronises) returning elapsed milliseconds */
 int fvb_timer_start(fvb_ctx* ctx);

@@ -320,9 +320,12 @@ def _run_device_step(state, cfg, piso):
     t0 = time.perf_counter()
     rc = fn(state._ctx.h, C.byref(scfg), _lib.ptr(sp), C.byref(rep))
     state._dev.invalidate()
+    state._last_solves = []
     for k in range(rep.n_solves):
         r = rep.rep[k]
         solver = "cg" if rep.solver[k] == 0 else "bicgstab"
+        # (solver, iterations, device seconds of the persistent solver kernel)
+        state._last_solves.append((solver, int(r.iterations), float(r.wall_time)))
         sc = cfg.pressure if solver == "cg" else cfg.momentum
         st = {}
         if sc.record_stages:

@@ -11,6 +11,7 @@
 #include "fvb_internal.cuh"
 
 static thread_local std::string g_last_error;
+unsigned long long fvb::g_launches = 0;
 
 void fvb_set_error(const char* fmt, ...) {
   char buf[1024];
@@ -235,14 +236,14 @@ __global__ void k_u_corr(int n, const double* hv, const double* rau, const doubl
 }
 
 int fill(Ctx* c, double* a, size_t n, double v) {
-  k_fill<<<grid_for(int64_t(n), kThreads), kThreads, 0, c->stream>>>(a, n, v);
+  { k_fill<<<grid_for(int64_t(n), kThreads), kThreads, 0, c->stream>>>(a, n, v); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int sumsq(Ctx* c, int ncomp, const double* x, double* out) {
   const int blocks = 2 * c->num_sms;
-  k_sumsq<<<blocks, kThreads, 0, c->stream>>>(c->nc, ncomp, x, c->partials);
+  { k_sumsq<<<blocks, kThreads, 0, c->stream>>>(c->nc, ncomp, x, c->partials); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   std::vector<double> h(3 * size_t(blocks));
   FVB_TRY(d2h(c, h.data(), c->partials, h.size()));
@@ -319,7 +320,7 @@ void fill_report(fvb_solve_report& r, const SolveOut& o) {
   r.converged = o.converged;
   r.initial_residual = o.res0;
   r.final_residual = o.res;
-  r.wall_time = 0.0;
+  r.wall_time = o.kernel_ms * 1e-3;
   r.error_iteration = o.error_iteration;
   r.error_kind = o.error_kind;
 }
@@ -364,11 +365,11 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   StepWork& w = work_of(c);
   const int n = c->nc;
   const int g = grid_for(n, kThreads);
-  k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag);
+  { k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag); fvb::note_launch(); }
   FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
   const bool relaxing = relax && cfg->alpha_u < 1.0;
-  k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, w.b0, c->vol, w.gp, w.diag, c->u, w.rhs, w.Vm,
-                                           c->diag_slot, relaxing, cfg->alpha_u);
+  { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, w.b0, c->vol, w.gp, w.diag, c->u, w.rhs, w.Vm,
+                                           c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   double bn2[3];
   FVB_TRY(sumsq(c, 3, w.rhs, bn2));
@@ -395,11 +396,10 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
       return out[k].error_kind == SE_TIMEOUT ? FVB_E_TIMEOUT : FVB_E_COUPLING;
     }
     FVB_TRY(log_solve(rep, 1, k, out[k]));
-    rep->rep[rep->n_solves - 1].wall_time = ev_ms(c, 2, 3) * 1e-3;
     worst = std::max(worst, out[k].res0 * bn[k] / bscale);
   }
   if (relaxing) {
-    k_set_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag);
+    { k_set_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag); fvb::note_launch(); }
     FVB_CUDA(cudaGetLastError());
   }
   rep->mom_res = worst;
@@ -415,7 +415,7 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
   FVB_CUDA(cudaEventRecord(c->ev[4], c->stream));
   MatView Am{w.Vm, w.crsm};
   for (int k = 0; k < 3; ++k) FVB_TRY(smvp(c, Am, c->u + size_t(k) * n, w.au + size_t(k) * n));
-  k_hbya<<<g, kThreads, 0, c->stream>>>(n, c->u, w.b0, w.au, w.diag, c->vol, w.hv, w.rau);
+  { k_hbya<<<g, kThreads, 0, c->stream>>>(n, c->u, w.b0, w.au, w.diag, c->vol, w.hv, w.rau); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(op_face_flux(c, 3, w.hv, c->ub, 0, w.phih));
   FVB_TRY(op_divergence(c, w.phih, w.divh));
@@ -433,10 +433,10 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
     if (corr) FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
     FVB_TRY(op_laplacian(c, 1, 1, Ap, w.rl, 0.0, w.rauf, c->p, c->pb, w.gp,
                          cfg->nonorth_correction, cfg->limiter, -1.0, w.coef, w.corr));
-    k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, w.rl, w.divh, w.rp);
+    { k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, w.rl, w.divh, w.rp); fvb::note_launch(); }
     if (cfg->pin_pressure)
-      k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, w.rp, cfg->pressure_ref_cell,
-                                    cfg->pressure_ref_value);
+      { k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, w.rp, cfg->pressure_ref_cell,
+                                    cfg->pressure_ref_value); fvb::note_launch(); }
     FVB_CUDA(cudaGetLastError());
     FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
     SolveOut o;
@@ -444,8 +444,7 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
     asm_ms += ev_ms(c, 6, 7);
     FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
     FVB_CUDA(cudaEventSynchronize(c->ev[6]));
-    const float this_solve = ev_ms(c, 7, 6);
-    solve_ms += this_solve;
+    solve_ms += ev_ms(c, 7, 6);
     if (o.error_kind != SE_NONE) {
       rep->failed_solve = rep->n_solves;
       std::string msg = solve_error_text("cg", o, o.error_iteration);
@@ -453,18 +452,17 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
       return o.error_kind == SE_TIMEOUT ? FVB_E_TIMEOUT : FVB_E_COUPLING;
     }
     FVB_TRY(log_solve(rep, 0, 3, o));
-    rep->rep[rep->n_solves - 1].wall_time = this_solve * 1e-3;
     if (*first_res < 0) *first_res = o.res0;
   }
   FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
   FVB_TRY(op_lap_flux(c, 1, 1, w.coef, w.corr, c->p, c->pb, w.lf));
-  k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux);
+  { k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux); fvb::note_launch(); }
   if (relax_p && cfg->alpha_p < 1.0)
-    k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, w.pbefore, cfg->alpha_p);
+    { k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, w.pbefore, cfg->alpha_p); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
   FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
-  k_u_corr<<<g, kThreads, 0, c->stream>>>(n, w.hv, w.rau, w.gp, c->u);
+  { k_u_corr<<<g, kThreads, 0, c->stream>>>(n, w.hv, w.rau, w.gp, c->u); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
   FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
@@ -538,6 +536,7 @@ int fvb_ctx_create(int device, fvb_ctx** out) {
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   for (auto& ev : c->tev) cudaEventCreate(&ev);
+  for (auto& ev : c->kev) cudaEventCreate(&ev);
   int rc = dalloc(c, &c->sync, 64);
   if (!rc) rc = dalloc(c, &c->partials, 16 * 4096 + 256);
   if (!rc) rc = dalloc(c, &c->ipart, 64);
@@ -559,6 +558,8 @@ int fvb_ctx_destroy(fvb_ctx* h) {
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : c->tev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : c->kev)
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   drop_ext(c);
@@ -873,11 +874,7 @@ static int solve_common(fvb_ctx* h, bool use_cg, int ncomp, const double* V, con
   FVB_CUDA(cudaEventRecord(c->ev[1], c->stream));
   FVB_TRY(d2h(c, x, dx, ncomp * n));
   FVB_TRY(sync(c));
-  const double wall = ev_ms(c, 0, 1) * 1e-3;
-  for (int k = 0; k < ncomp; ++k) {
-    fill_report(reps[k], out[k]);
-    reps[k].wall_time = wall;
-  }
+  for (int k = 0; k < ncomp; ++k) fill_report(reps[k], out[k]);
   for (int k = 0; k < ncomp; ++k) {
     if (out[k].error_kind != SE_NONE) {
       std::string msg = solve_error_text(use_cg ? "cg" : "bicgstab", out[k], out[k].error_iteration);
@@ -1116,7 +1113,7 @@ int fvb_continuity_error(fvb_ctx* h, double* out) {
   }
   FVB_TRY(op_divergence(c, c->flux, div));
   const int blocks = 2 * c->num_sms;
-  k_absmax<<<blocks, kThreads, 0, c->stream>>>(c->nc, div, c->partials);
+  { k_absmax<<<blocks, kThreads, 0, c->stream>>>(c->nc, div, c->partials); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   std::vector<double> hm(blocks);
   FVB_TRY(d2h(c, hm.data(), c->partials, size_t(blocks)));
@@ -1139,6 +1136,20 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
   Ctx* c = &h->c;
   cudaSetDevice(c->dev);
   return run_step(c, cfg, u_speeds, rep, false);
+}
+
+unsigned long long fvb_launch_count(void) { return g_launches; }
+
+int fvb_host_register(void* ptr, int64_t bytes) {
+  if (!ptr || bytes <= 0) return FVB_OK;
+  FVB_CUDA(cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterDefault));
+  return FVB_OK;
+}
+
+int fvb_host_unregister(void* ptr) {
+  if (!ptr) return FVB_OK;
+  FVB_CUDA(cudaHostUnregister(ptr));
+  return FVB_OK;
 }
 
 int fvb_timer_start(fvb_ctx* h) {

@@ -32,6 +32,10 @@ namespace fvb {
 
 constexpr int kMaxK = 16;
 
+// host-side count of kernel launches issued by libfvb (fvb_launch_count)
+extern unsigned long long g_launches;
+inline void note_launch() { ++g_launches; }
+
 // ------------------------------------------------------------ device views
 // Face numbering follows the reference: internal faces [0, ni), boundary
 // faces [ni, nf); boundary arrays are indexed j = f - ni.
@@ -91,6 +95,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8];
   cudaEvent_t tev[2];
+  cudaEvent_t kev[2];
   int64_t bytes = 0;
   bool have_mesh = false, have_pattern = false;
   bool have_bc[2] = {false, false};
@@ -303,6 +308,7 @@ int smvp(Ctx* c, MatView A, const double* x, double* y);
 struct SolveOut {
   int iterations, converged, error_kind, error_iteration;
   double res0, res;
+  double kernel_ms;  // device time of the persistent solver kernel alone
 };
 enum SolveErr {
   SE_NONE = 0,

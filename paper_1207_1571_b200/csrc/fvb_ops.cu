@@ -424,24 +424,24 @@ __global__ void k_smvp(PatternView P, const double* __restrict__ V, const double
 // ------------------------------------------------------------ launchers
 int op_precompute_geometry(Ctx* c, const double* dx, const double* dy, const double* dz,
                            const double* dbx, const double* dby, const double* dbz) {
-  k_precompute<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
-      c->mesh(), c->a, c->kx, c->ky, c->kz, dx, dy, dz, dbx, dby, dbz);
+  { k_precompute<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
+      c->mesh(), c->a, c->kx, c->ky, c->kz, dx, dy, dz, dbx, dby, dbz); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int op_apply_bcs(Ctx* c, int field, int ncomp, const double* vals, double* bnd) {
   if (c->nb == 0) return FVB_OK;
-  k_apply_bcs<<<grid_for(c->nb, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field), ncomp,
-                                                                     vals, bnd);
+  { k_apply_bcs<<<grid_for(c->nb, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field), ncomp,
+                                                                     vals, bnd); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int op_interp(Ctx* c, int field, int ncomp, const double* vals, const double* bnd, double* fv) {
   BcView B = field >= 0 ? c->bc(field) : BcView{nullptr, nullptr, nullptr, nullptr};
-  k_interp<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), B, field < 0, ncomp,
-                                                                   vals, bnd, fv);
+  { k_interp<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), B, field < 0, ncomp,
+                                                                   vals, bnd, fv); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
@@ -449,17 +449,17 @@ int op_interp(Ctx* c, int field, int ncomp, const double* vals, const double* bn
 int op_gradient(Ctx* c, int field, int ncomp, const double* vals, const double* bnd,
                 double* grad) {
   if (ncomp == 1)
-    k_gradient<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
-                                                                         vals, bnd, grad);
+    { k_gradient<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
+                                                                         vals, bnd, grad); fvb::note_launch(); }
   else
-    k_gradient<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
-                                                                         vals, bnd, grad);
+    { k_gradient<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
+                                                                         vals, bnd, grad); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int op_divergence(Ctx* c, const double* flux, double* div) {
-  k_divergence<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), flux, div);
+  { k_divergence<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), flux, div); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
@@ -479,17 +479,17 @@ int op_laplacian(Ctx* c, int field, int ncomp, MatView A, double* rhs, double ga
   }
   LapArgs L{gamma, gamma_faces, coeff, nonorth && limiter > 0.0, limiter};
   if (ncomp == 1) {
-    k_laplacian_rows<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
-        c->mesh(), c->pattern(), c->bc(field), L, A, rhs, bnd, grad);
+    { k_laplacian_rows<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+        c->mesh(), c->pattern(), c->bc(field), L, A, rhs, bnd, grad); fvb::note_launch(); }
     if (coef)
-      k_laplacian_faces<1><<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
-          c->mesh(), c->bc(field), L, grad, coef, corr);
+      { k_laplacian_faces<1><<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
+          c->mesh(), c->bc(field), L, grad, coef, corr); fvb::note_launch(); }
   } else {
-    k_laplacian_rows<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
-        c->mesh(), c->pattern(), c->bc(field), L, A, rhs, bnd, grad);
+    { k_laplacian_rows<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+        c->mesh(), c->pattern(), c->bc(field), L, A, rhs, bnd, grad); fvb::note_launch(); }
     if (coef)
-      k_laplacian_faces<3><<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
-          c->mesh(), c->bc(field), L, grad, coef, corr);
+      { k_laplacian_faces<3><<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
+          c->mesh(), c->bc(field), L, grad, coef, corr); fvb::note_launch(); }
   }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
@@ -497,8 +497,8 @@ int op_laplacian(Ctx* c, int field, int ncomp, MatView A, double* rhs, double ga
 
 int op_lap_flux(Ctx* c, int field, int ncomp, const double* coef, const double* corr,
                 const double* vals, const double* bnd, double* out) {
-  k_lap_flux<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field), ncomp,
-                                                                    coef, corr, vals, bnd, out);
+  { k_lap_flux<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field), ncomp,
+                                                                    coef, corr, vals, bnd, out); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
@@ -506,19 +506,19 @@ int op_lap_flux(Ctx* c, int field, int ncomp, const double* coef, const double* 
 int op_convection(Ctx* c, int field, int ncomp, MatView A, double* rhs, const double* flux,
                   const double* bnd, int scheme, double coeff) {
   if (ncomp == 1)
-    k_convection_rows<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
-        c->mesh(), c->pattern(), c->bc(field), A, rhs, flux, bnd, scheme, coeff);
+    { k_convection_rows<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+        c->mesh(), c->pattern(), c->bc(field), A, rhs, flux, bnd, scheme, coeff); fvb::note_launch(); }
   else
-    k_convection_rows<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
-        c->mesh(), c->pattern(), c->bc(field), A, rhs, flux, bnd, scheme, coeff);
+    { k_convection_rows<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+        c->mesh(), c->pattern(), c->bc(field), A, rhs, flux, bnd, scheme, coeff); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int op_ddt(Ctx* c, int ncomp, MatView A, double* rhs, const double* old, double dt,
            double coeff) {
-  k_ddt<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->nc, c->pattern(), A, ncomp, rhs,
-                                                               old, c->vol, dt, coeff);
+  { k_ddt<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->nc, c->pattern(), A, ncomp, rhs,
+                                                               old, c->vol, dt, coeff); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
@@ -526,15 +526,15 @@ int op_ddt(Ctx* c, int ncomp, MatView A, double* rhs, const double* old, double 
 int op_face_flux(Ctx* c, int ncomp_field, const double* vals, const double* bnd,
                  int field_for_mask, double* flux) {
   (void)ncomp_field;
-  k_face_flux<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field_for_mask),
-                                                                     vals, bnd, flux);
+  { k_face_flux<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field_for_mask),
+                                                                     vals, bnd, flux); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int launch_inv_diag(Ctx* c, const double* V, double* inv, int* first_zero) {
-  k_inv_diag<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->nc, c->diag_slot, V, inv,
-                                                                     first_zero);
+  { k_inv_diag<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->nc, c->diag_slot, V, inv,
+                                                                     first_zero); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
@@ -543,9 +543,9 @@ int smvp(Ctx* c, MatView A, const double* x, double* y) {
   PatternView P = c->pattern();
   const int g = grid_for(c->nc, kThreads);
   switch (c->k) {
-    case 5: k_smvp<5><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); break;
-    case 7: k_smvp<7><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); break;
-    default: k_smvp<0><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); break;
+    case 5: { k_smvp<5><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
+    case 7: { k_smvp<7><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
+    default: { k_smvp<0><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
   }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;

@@ -505,6 +505,7 @@ int coop_launch(Ctx* c, K kernel, Args& args) {
   FVB_TRY(coop_blocks(c, kernel, &blocks));
   FVB_CUDA(cudaMemsetAsync(c->sync, 0, 4 * sizeof(unsigned), c->stream));
   void* params[] = {&args};
+  fvb::note_launch();
   FVB_CUDA(cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads),
                                        params, 0, c->stream));
   return FVB_OK;
@@ -565,7 +566,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
   FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
-  *out = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0};
+  *out = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0};
   if (zero_row != 0x7fffffff) {
     out->error_kind = SE_ZERO_DIAG;
     out->error_iteration = zero_row;
@@ -573,11 +574,13 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   }
   CgParams prm{c->pattern(), A.V, A.crs, inv, b, x, r, pa, pb, q, tol, abs_tol, max_iters,
                c->sync, c->partials, result};
+  FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
   switch (c->k) {
     case 5: FVB_TRY(coop_launch(c, k_cg<5>, prm)); break;
     case 7: FVB_TRY(coop_launch(c, k_cg<7>, prm)); break;
     default: FVB_TRY(coop_launch(c, k_cg<0>, prm)); break;
   }
+  FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[6];
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof h, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
@@ -587,6 +590,9 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   out->res = h[3];
   out->error_kind = int(h[4]);
   out->error_iteration = int(h[5]);
+  float kms = 0.f;
+  FVB_CUDA(cudaEventElapsedTime(&kms, c->kev[0], c->kev[1]));
+  out->kernel_ms = kms;
   return FVB_OK;
 }
 
@@ -631,20 +637,22 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
   FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
-  for (int k = 0; k < ncomp; ++k) out[k] = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0};
+  for (int k = 0; k < ncomp; ++k) out[k] = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0};
   if (zero_row != 0x7fffffff) {
     out[0].error_kind = SE_ZERO_DIAG;
     out[0].error_iteration = zero_row;
     return FVB_OK;
   }
-  if (ncomp == 1)
-    FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
-  else if (ncomp == 3)
-    FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
-  else {
+  if (ncomp != 1 && ncomp != 3) {
     fvb_set_error("bicgstab batch supports 1 or 3 components");
     return FVB_E_ARG;
   }
+  FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
+  if (ncomp == 1)
+    FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  else
+    FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[18];
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof(double) * 6 * ncomp, cudaMemcpyDeviceToHost,
                            c->stream));
@@ -657,6 +665,9 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
     out[k].error_kind = int(h[6 * k + 4]);
     out[k].error_iteration = int(h[6 * k + 5]);
   }
+  float kms = 0.f;
+  FVB_CUDA(cudaEventElapsedTime(&kms, c->kev[0], c->kev[1]));
+  for (int k = 0; k < ncomp; ++k) out[k].kernel_ms = kms;
   return FVB_OK;
 }
 
