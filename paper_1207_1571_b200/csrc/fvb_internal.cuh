@@ -30,7 +30,7 @@
 
 namespace fvb {
 
-constexpr int kMaxK = 16;
+constexpr int kMaxK = 1 << 20;  // K is a runtime bound on the generic path
 
 // host-side count of kernel launches issued by libfvb (fvb_launch_count)
 extern unsigned long long g_launches;
@@ -172,7 +172,7 @@ __device__ __forceinline__ double ell_row(const double* __restrict__ V,
   const int K = KT > 0 ? KT : kdyn;
   double ev = 0.0, od = 0.0;
 #pragma unroll
-  for (int s = 0; s < (KT > 0 ? KT : kMaxK); s += 2) {
+  for (int s = 0; s < (KT > 0 ? KT : K); s += 2) {
     if (KT == 0 && s >= K) break;
     int col = __ldg(I + size_t(s) * n + i);
     double v = __ldg(V + size_t(s) * n + i);
@@ -180,7 +180,7 @@ __device__ __forceinline__ double ell_row(const double* __restrict__ V,
     ev = (s == 0) ? pr : ev + pr;
   }
 #pragma unroll
-  for (int s = 1; s < (KT > 0 ? KT : kMaxK); s += 2) {
+  for (int s = 1; s < (KT > 0 ? KT : K); s += 2) {
     if (KT == 0 && s >= K) break;
     int col = __ldg(I + size_t(s) * n + i);
     double v = __ldg(V + size_t(s) * n + i);

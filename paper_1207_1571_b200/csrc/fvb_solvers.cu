@@ -179,7 +179,7 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
 #pragma unroll
   for (int c = 0; c < NC; ++c) ev[c] = od[c] = 0.0;
 #pragma unroll
-  for (int s = 0; s < (KT > 0 ? KT : kMaxK); s += 2) {
+  for (int s = 0; s < (KT > 0 ? KT : K); s += 2) {
     if (KT == 0 && s >= K) break;
     int col = __ldg(P.I + size_t(s) * n + i);
     col = col < 0 ? 0 : col;
@@ -192,7 +192,7 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
       }
   }
 #pragma unroll
-  for (int s = 1; s < (KT > 0 ? KT : kMaxK); s += 2) {
+  for (int s = 1; s < (KT > 0 ? KT : K); s += 2) {
     if (KT == 0 && s >= K) break;
     int col = __ldg(P.I + size_t(s) * n + i);
     col = col < 0 ? 0 : col;
