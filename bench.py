@@ -1,25 +1,34 @@
 """Benchmark: FP64 PISO time steps of the 3D lid-driven cavity on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c2|c5] [--n CELLS_PER_EDGE]
+                    [--config c5|c2] [--n CELLS_PER_EDGE]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
 
-Workload (BASELINE.json configs[1], "C2"): gen_cavity(128) (2,097,152 hex
-cells, K = 7), PISO with the reference defaults (cg_tol 1e-10,
-bicgstab_tol 1e-8, max_iters 2000, 2 correctors), dt = 0.1/128 (Co = 1),
-from rest; W warm-up steps, then K timed steps.  The working set (matrix,
-pattern, Krylov vectors: ~1.4 GB) is larger than the 126 MB L2, so no
+Workload (default "C5", BASELINE.json configs[4] and the north-star target
+config): gen_cavity(256) = 16,777,216 hex cells (K = 7), PISO with the
+reference defaults except max_iters = 5000 (the 2000 cap binds at 256^3,
+SURVEY.md §7 hard part 2 / §8(d) C5), dt = 0.1/256 (Co = 1), from rest.
+The same mesh is used at every N (strong scaling): N ranks own N z-slabs
+(decompose.py) and exchange halos / reduction partials inside the kernels
+over NVLink peer memory.  --config c2 selects gen_cavity(128) (configs[1]).
+The device working set (~19 GB at 256^3) dwarfs the 126 MB L2, so no L2
 flush is needed between steps.
 
 One JSON line on rank 0:
-  value        cell-updates/s = cells / (device ms per step), device-resident
-  e2e          same metric through the C ABI with pinned HOST buffers: each
-               step uploads u, p, flux and downloads them again
-  roofline     the dominant kernel (persistent Jacobi-PCG, k_cg): algorithmic
-               bytes per launch N(12K+80) + iters*N(12K+96)
-               over its CUDA-event duration, against MEASURED_PEAKS hbm_gbs
-  cpu_baseline the reference fvflow (baseline/_ref, unmodified) on a bounded
-               sample of the same step, extrapolated with the step's counts
---impl reference prints the reference arm's line (CPU, no GPU work).
+  value        cell-updates/s = cells / (device ms per step, max over ranks)
+  e2e          the same metric through the public API with HOST buffers:
+               every step uploads u, p, flux from pinned memory and
+               downloads them again (bytes counted per step, all ranks)
+  roofline     dominant kernel = persistent Jacobi-PCG (k_cg): algorithmic
+               bytes N(12K+80) + iters * N(12K+96) per launch (SURVEY.md
+               §8(d)) over its CUDA-event duration; peak = MEASURED_PEAKS
+               hbm_gbs x N GPUs; traffic = ncu DRAM bytes per launch scaled
+               from profiles/ncu_k_cg_traffic.json
+  cpu_baseline the unmodified reference fvflow (baseline/_ref) on a bounded
+               sample: one piso_time_step on gen_cavity(min(n,128)) with CG
+               and BiCGStab capped, per-cell costs scaled to this workload
+               and to this run's iteration counts
+--impl reference prints the reference arm's line (CPU, rank 0 only).
 """
 
 import argparse
@@ -38,6 +47,7 @@ sys.path.insert(0, HERE)
 
 HBM_FALLBACK = 6650.0  # B200_PROFILING.md fallback, only if MEASURED_PEAKS.json is absent
 REF_DIR = os.path.join(HERE, "baseline", "_ref")
+METRIC = "cell-updates/s (FP64 PISO time step)"
 # reference iteration counts of gen_cavity(128) PISO step 2 measured on the
 # reference itself: CG 1494 + 1510, BiCGStab 65 + 62 + 66
 REF_COUNTS_C2 = {"cg": 3004, "cg_solves": 2, "bicgstab": 193, "bicgstab_solves": 3}
@@ -49,16 +59,16 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c2", "c5"])
     ap.add_argument("--n", type=int, default=0, help="override cells per edge")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cg-sample", type=int, default=20)
     return ap.parse_args()
 
 
 def workload(args):
-    n = args.n or (128 if args.config == "c2" else 256)
-    return n
+    return args.n or (128 if args.config == "c2" else 256)
 
 
 def peaks():
@@ -143,14 +153,18 @@ def _ref_modules():
 
 
 class RefSampler:
-    """Bounded samples of the reference's own piso_time_step on the same
-    workload.  The reference objects are built from this package's setup
-    arrays, which are bit-identical to the reference's own compute_geometry
-    / build_pattern (tests/test_native_setup.py) — that skips its 30-50 s
-    numpy setup.  Each sample is one reference step with CG capped at cg_cap
-    and BiCGStab at bi_cap iterations per solve: assembly and correction
-    are timed in full, solver time per iteration is scaled to the full
-    step's iteration counts."""
+    """Bounded samples of the reference's own piso_time_step.
+
+    The reference objects are built from this package's setup arrays, which
+    are bit-identical to the reference's compute_geometry / build_pattern
+    (tests/test_native_setup.py); that skips 30-50 s of numpy setup.  One
+    sample = one reference step with CG capped at cg_cap and BiCGStab at
+    bi_cap iterations per solve: assembly and correction are timed in
+    full, the solver time per iteration is measured, and the step is
+    assembled from the target's iteration counts.  When the target mesh is
+    larger than the sample mesh, every term is scaled by the cell ratio
+    (numpy costs here are linear in N; SURVEY.md §6/§8(d) C5 prescribes
+    this extrapolation because 256^3 needs ~77 GB in the reference)."""
 
     def __init__(self, case, seed=None, cg_cap=20, bi_cap=10):
         mods = _ref_modules()
@@ -189,10 +203,10 @@ class RefSampler:
         self.state = rc.RunState(mesh=rmesh, geom=geom, pattern=self.pat, u=u, p=p, flux=flux,
                                  pin_pressure=True)
         self.start = (u.values.copy(), p.values.copy(), flux.copy(),
-                      seed["outer"] if seed is not None else 0)
+                      seed["outer"] if seed is not None else 1)
         self.n = m.n_cells
 
-    def sample(self, counts):
+    def sample(self, counts, n_target):
         rc, rs, st = self.rc, self.rs, self.state
         st.u.values = self.start[0].copy()
         st.p.values = self.start[1].copy()
@@ -218,30 +232,31 @@ class RefSampler:
                  + w.get("correction", 0.0))
         t_step = (fixed + counts["cg_solves"] * t_smvp + counts["cg"] * t_cg_iter
                   + counts["bicgstab_solves"] * t_smvp + counts["bicgstab"] * t_bi_iter)
-        return {"s_per_step": t_step, "sample_s": t_sample, "t_cg_iter_s": t_cg_iter,
+        scale = n_target / self.n
+        return {"s_per_step": t_step * scale, "sample_s": t_sample, "t_cg_iter_s": t_cg_iter,
                 "t_bicgstab_iter_s": t_bi_iter, "t_smvp_s": t_smvp,
-                "assembly_correction_s": fixed,
+                "assembly_correction_s": fixed, "sample_cells": self.n, "cell_scale": scale,
                 "sampled_iters": {"cg": cg_it, "bicgstab": bi_it}, "counts": counts,
                 "threads": os.environ.get("OPENBLAS_NUM_THREADS", "default")}
 
 
-def reference_sample(case, counts, seed=None, cg_cap=20, bi_cap=10):
-    s = RefSampler(case, seed, cg_cap, bi_cap)
-    return s.sample(counts) if s.ok else None
+def _sample_case(n):
+    """The reference sample mesh: the workload itself up to 128^3, else 128^3."""
+    return make_case(min(n, 128))
+
+
+def _default_counts(n):
+    if n == 128:
+        return dict(REF_COUNTS_C2)
+    f = n / 128  # CG iterations grow ~2x per doubling of n (SURVEY.md §7)
+    return {"cg": int(3004 * f), "cg_solves": 2, "bicgstab": int(193 * f), "bicgstab_solves": 3}
 
 
 def run_reference(args):
     n = workload(args)
-    case = make_case(n)
-    N = case.mesh.n_cells
-    counts = dict(REF_COUNTS_C2)
-    if n != 128:  # scale counts like the CG iteration growth (~2x per doubling)
-        f = n / 128
-        counts = {"cg": int(3004 * f), "cg_solves": 2, "bicgstab": int(193 * f),
-                  "bicgstab_solves": 3}
-    times = []
-    detail = None
-    sampler = RefSampler(case, cg_cap=args.cg_sample)
+    N = n ** 3
+    counts = _default_counts(n)
+    sampler = RefSampler(_sample_case(n), cg_cap=args.cg_sample)
     if not sampler.ok:
         print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref/fvflow not installed"}))
         return
@@ -249,26 +264,28 @@ def run_reference(args):
     A = sampler.rs.HybridMatrix.zeros(sampler.pat)
     for _ in range(args.warmup):
         sampler.rs.smvp(A, np.ones(sampler.n))
+    times = []
+    detail = None
     for _ in range(args.steps):
-        d = sampler.sample(counts)
+        d = sampler.sample(counts, N)
         times.append(d["s_per_step"])
         detail = d
     ms = 1e3 * statistics.mean(times)
     value = N / (ms / 1e3)
-    sample = (f"reference fvflow piso_time_step on gen_cavity({n}); CG capped at "
-              f"{args.cg_sample} and BiCGStab at 10 iterations per solve, assembly and "
-              f"correction timed in full; per-iteration costs scaled to the reference's own "
-              f"step-2 counts (CG {counts['cg']}, BiCGStab {counts['bicgstab']}, SURVEY.md §6)")
-    cores = os.cpu_count()
+    sample = (f"reference fvflow piso_time_step on gen_cavity({min(n, 128)}) from rest+1 step, "
+              f"CG capped at {args.cg_sample} and BiCGStab at 10 iterations per solve, assembly "
+              f"and correction timed in full; per-iteration costs scaled to CG {counts['cg']} / "
+              f"BiCGStab {counts['bicgstab']} iterations per step and by {N / sampler.n:g}x cells "
+              f"to gen_cavity({n})")
     out = {
-        "metric": "cell-updates/s (FP64 PISO time step)", "impl": "reference",
+        "metric": METRIC, "impl": "reference",
         "value": value, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (gen_cavity mesh, from rest)",
-        "config": {"workload": f"C2 gen_cavity({n}) PISO dt=0.1/{n}", "cells": N,
+        "data": "synthetic (gen_cavity mesh, PISO)",
+        "config": {"workload": f"gen_cavity({n}) PISO dt=0.1/{n}", "cells": N,
                    "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": cores,
+        "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": os.cpu_count(),
                          "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -278,118 +295,184 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+class _Dist:
+    """Rank plumbing: torch.distributed (gloo) for objects and max-over-ranks."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.dist = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def allgather(self, obj):
+        if self.dist is None:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+
+    def max(self, v):
+        return max(self.allgather(float(v)))
+
+    def sum(self, v):
+        return sum(self.allgather(float(v)))
+
+    def close(self):
+        if self.dist is not None:
+            self.dist.destroy_process_group()
+
+
 def run_ours(args):
     import ctypes as C
 
     from paper_1207_1571_b200 import _lib
     from paper_1207_1571_b200.coupling import CouplingConfig, init_state, piso_time_step
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
-        raise SystemExit("multi-GPU domain decomposition is not wired into bench.py yet")
+    D = _Dist()
     n = workload(args)
     t_setup = time.perf_counter()
     case = make_case(n)
     cfg = CouplingConfig.from_case_config(case.config)
-    st = init_state(case, cfg)
-    t_setup = time.perf_counter() - t_setup
     mesh = case.mesh
     N, F = mesh.n_cells, mesh.n_faces
-    K = st.pattern.k
-    h = st._ctx.h
+    if D.world > 1:
+        from paper_1207_1571_b200.team import RankRun
+
+        run = RankRun(case, cfg, D.rank, D.world, D.local, D.allgather)
+        h = run.ctx.h
+        step = lambda: run.piso_time_step(cfg)  # noqa: E731
+        last_solves = lambda: run.last_solves  # noqa: E731
+        log = run.residual_log
+        K = run.pattern.k
+        n_local = run.member.sd.n_rows
+        dev_bytes = run.ctx.device_bytes
+    else:
+        st = init_state(case, cfg)
+        h = st._ctx.h
+        step = lambda: piso_time_step(st, cfg)  # noqa: E731
+        last_solves = lambda: st._last_solves  # noqa: E731
+        log = st.residual_log
+        K = st.pattern.k
+        n_local = N
+        dev_bytes = st._ctx.device_bytes
+    t_setup = time.perf_counter() - t_setup
     for _ in range(args.warmup):
-        piso_time_step(st, cfg)
-    # seed for the CPU reference sample: the state the timed steps start from
+        step()
     seed = None
-    if not args.no_cpu_baseline:
+    if D.world == 1 and not args.no_cpu_baseline:
         seed = {"u": st.u.values.copy(), "p": st.p.values.copy(), "flux": st.flux.copy(),
                 "outer": st.outer}
         st._dev.host_dirty.clear()
-    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
-    nlog = len(st.residual_log)
+    clocks = ClockSampler(D.local) if D.rank == 0 else None
+    nlog = len(log)
     l0 = _lib.lib.fvb_launch_count()
     _lib.check(_lib.lib.fvb_sync(h))
+    D.barrier()
     _lib.check(_lib.lib.fvb_timer_start(h))
     kernel_rows = []
     for _ in range(args.steps):
-        piso_time_step(st, cfg)
-        kernel_rows.extend(st._last_solves)
+        step()
+        kernel_rows.extend(last_solves())
     ms = C.c_double()
     _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
-    launches = _lib.lib.fvb_launch_count() - l0
-    clk = clocks.stop()
-    ms_step = ms.value / args.steps
-    rows = st.residual_log[nlog:]
+    launches = int(_lib.lib.fvb_launch_count() - l0)
+    clk = clocks.stop() if clocks else None
+    ms_step = D.max(ms.value) / args.steps
+    rows = log[nlog:]
     cg_iters = [r[3] for r in rows if r[0] == "cg"]
     bi_iters = [r[3] for r in rows if r[0] == "bicgstab"]
-    # dominant kernel: persistent PCG (k_cg)
+    # dominant kernel: persistent PCG (k_cg), bytes of this rank's rows
     cg_k = [(it, ks) for (solver, it, ks) in kernel_rows if solver == "cg"]
-    b_setup = N * (12 * K + 80)
-    b_iter = N * (12 * K + 96)
-    cg_bytes = sum(b_setup + it * b_iter for it, _ in cg_k)
-    cg_time = sum(ks for _, ks in cg_k)
-    peak, peak_kind = peaks()
+    b_setup = n_local * (12 * K + 80)
+    b_iter = n_local * (12 * K + 96)
+    cg_bytes = D.sum(sum(b_setup + it * b_iter for it, _ in cg_k))
+    cg_time = D.max(sum(ks for _, ks in cg_k))
+    peak1, peak_kind = peaks()
+    peak = peak1 * D.world
     achieved = cg_bytes / cg_time / 1e9 if cg_time > 0 else 0.0
+    mean_iters = sum(it for it, _ in cg_k) / max(len(cg_k), 1)
     traffic = None
     prof = os.path.join(HERE, "profiles", "ncu_k_cg_traffic.json")
     if os.path.exists(prof):
         with open(prof) as f:
             pj = json.load(f)
-        traffic = pj.get("bytes_per_launch")
+        bpr = pj.get("bytes_per_row_iteration")
+        if bpr:
+            traffic = bpr * N * mean_iters  # per launch, all ranks
     # whole-step algorithmic bytes (SURVEY §8(d)): solves + ~3.2 kB/cell FV work
-    bi_max = []
-    per = 3
-    for i in range(0, len(bi_iters), per):
-        bi_max.append(max(bi_iters[i:i + per]))
-    step_bytes = (cg_bytes + sum(bi_iters) * 160 * N + sum(bi_max) * 24 * K * N
+    bi_max = [max(bi_iters[i:i + 3]) for i in range(0, len(bi_iters), 3)]
+    step_bytes = ((sum(b_setup + it * b_iter for it, _ in cg_k) / n_local) * N
+                  + sum(bi_iters) * 160 * N + sum(bi_max) * 24 * K * N
                   + len(bi_max) * 3 * N * (12 * K + 56) + args.steps * 3200 * N)
-    step_gbs = step_bytes / (ms.value / 1e3) / 1e9
+    step_gbs = step_bytes / (ms_step * args.steps / 1e3) / 1e9
     # ---------------------------------------------------------------- e2e
-    u_h = np.ascontiguousarray(st.u.values.T).reshape(-1).copy()
-    p_h = st.p.values.copy()
-    f_h = st.flux.copy()
-    st._dev.host_dirty.clear()
-    bufs = (u_h, p_h, f_h)
-    for b in bufs:
-        _lib.check(_lib.lib.fvb_host_register(b.ctypes.data, b.nbytes))
-    P = _lib.ptr
-    scfg_state = st
-    _lib.check(_lib.lib.fvb_sync(h))
-    _lib.check(_lib.lib.fvb_timer_start(h))
-    for _ in range(args.steps):
-        _lib.check(_lib.lib.fvb_set_state(h, P(u_h), P(p_h), P(f_h), None, None))
-        piso_time_step(scfg_state, cfg)
-        _lib.check(_lib.lib.fvb_get_state(h, P(u_h), P(p_h), P(f_h), None, None))
-    e2e_ms = C.c_double()
-    _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(e2e_ms)))
-    for b in bufs:
-        _lib.lib.fvb_host_unregister(b.ctypes.data)
-    e2e_step = e2e_ms.value / args.steps
-    io_bytes = sum(b.nbytes for b in bufs)
+    e2e = None
+    if not args.no_e2e:
+        if D.world > 1:
+            u_h, p_h, f_h = (np.ascontiguousarray(a) for a in run.local_state())
+            u_h = np.ascontiguousarray(u_h.T).reshape(-1).copy()
+        else:
+            u_h = np.ascontiguousarray(st.u.values.T).reshape(-1).copy()
+            p_h = st.p.values.copy()
+            f_h = st.flux.copy()
+            st._dev.host_dirty.clear()
+        bufs = (u_h, p_h, f_h)
+        for b in bufs:
+            _lib.check(_lib.lib.fvb_host_register(b.ctypes.data, b.nbytes))
+        P = _lib.ptr
+        _lib.check(_lib.lib.fvb_sync(h))
+        D.barrier()
+        _lib.check(_lib.lib.fvb_timer_start(h))
+        for _ in range(args.steps):
+            _lib.check(_lib.lib.fvb_set_state(h, P(u_h), P(p_h), P(f_h), None, None))
+            step()
+            _lib.check(_lib.lib.fvb_get_state(h, P(u_h), P(p_h), P(f_h), None, None))
+        e2e_ms = C.c_double()
+        _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(e2e_ms)))
+        for b in bufs:
+            _lib.lib.fvb_host_unregister(b.ctypes.data)
+        e2e_step = D.max(e2e_ms.value) / args.steps
+        io_bytes = int(D.sum(sum(b.nbytes for b in bufs)))
+        e2e = {"value": N / (e2e_step / 1e3), "unit": "cell-updates/s",
+               "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+               "ms_per_step": e2e_step}
     # ------------------------------------------------------- cpu baseline
     cpu = None
     if seed is not None:
-        counts = {"cg": statistics.mean(cg_iters) * 2 if cg_iters else 0,
-                  "cg_solves": 2,
-                  "bicgstab": sum(bi_iters) / max(args.steps, 1),
-                  "bicgstab_solves": 3}
-        d = reference_sample(case, counts, seed=seed, cg_cap=args.cg_sample)
-        if d is not None:
+        counts = {"cg": sum(cg_iters) / args.steps, "cg_solves": 2,
+                  "bicgstab": sum(bi_iters) / args.steps, "bicgstab_solves": 3}
+        if n <= 128:
+            s = RefSampler(case, seed=seed, cg_cap=args.cg_sample)
+            where = "the same state as the timed steps"
+        else:
+            s = RefSampler(_sample_case(n), cg_cap=args.cg_sample)
+            where = f"rest on gen_cavity({min(n, 128)}), scaled by {N / min(n, 128) ** 3:g}x cells"
+        if s.ok:
+            d = s.sample(counts, N)
             cpu = {"value": N / d["s_per_step"], "unit": "cell-updates/s",
                    "cores": os.cpu_count(), "kind": "reference",
                    "sample": (f"unmodified reference fvflow (baseline/_ref) piso_time_step from "
-                              f"the same state as the timed steps, CG capped at "
-                              f"{args.cg_sample} and BiCGStab at 10 iterations; assembly and "
-                              f"correction timed in full, per-iteration solver cost scaled to "
-                              f"this run's mean counts (CG {counts['cg']:.0f}, BiCGStab "
-                              f"{counts['bicgstab']:.0f} per step); OpenBLAS default threads; "
-                              f"{d['sample_s']:.1f} s of CPU work"),
+                              f"{where}; CG capped at {args.cg_sample} and BiCGStab at 10 "
+                              f"iterations; assembly and correction timed in full, per-iteration "
+                              f"solver cost scaled to this run's mean counts (CG "
+                              f"{counts['cg']:.0f}, BiCGStab {counts['bicgstab']:.0f} per step); "
+                              f"OpenBLAS default threads; {d['sample_s']:.1f} s of CPU work"),
                    "s_per_step": d["s_per_step"]}
     out = {
-        "metric": "cell-updates/s (FP64 PISO time step)",
+        "metric": METRIC,
         "value": N / (ms_step / 1e3),
         "unit": "cell-updates/s",
-        "n_gpus": 1,
+        "n_gpus": D.world,
         "steps": args.steps,
         "warmup": args.warmup,
         "ms_per_step": ms_step,
@@ -398,29 +481,32 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (gen_cavity mesh, PISO from rest; steps W+1..W+K timed)",
-        "config": {"workload": f"C2 gen_cavity({n}) PISO dt=0.1/{n} (Co=1), reference defaults",
-                   "cells": N, "faces": F, "K": K, "parallelism": "single",
-                   "l2": "inputs larger than L2 (device working set "
-                         f"{st._ctx.device_bytes / 1e9:.2f} GB > 126 MB L2)",
+        "config": {"workload": (f"{'C5' if n == 256 else 'C2' if n == 128 else 'cavity'} "
+                                f"gen_cavity({n}) PISO dt=0.1/{n} (Co=1), reference defaults"
+                                + (", max_iters 5000" if n > 128 else "")),
+                   "cells": N, "faces": F, "K": K,
+                   "parallelism": (f"domain decomposition, {D.world} z-slabs" if D.world > 1
+                                   else "single"),
+                   "l2": ("inputs larger than L2 (device working set "
+                          f"{dev_bytes / 1e9:.2f} GB per GPU > 126 MB L2)"),
                    "setup_s": round(t_setup, 2)},
-        "e2e": {"value": N / (e2e_step / 1e3), "unit": "cell-updates/s",
-                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
-                "ms_per_step": e2e_step},
+        "e2e": e2e,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "kernel": "k_cg (persistent PCG)",
-                     "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_cg (persistent Jacobi-PCG)", "peak_kind": peak_kind,
                      "bytes_model": f"N*(12K+80) + iters*N*(12K+96), K={K}",
-                     "launches": len(cg_k), "mean_iters": cg_bytes and
-                     sum(it for it, _ in cg_k) / max(len(cg_k), 1)},
+                     "launches": len(cg_k), "mean_iters": mean_iters},
         "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
                      "bytes_per_step": step_bytes / args.steps},
         "iterations_per_step": {"cg": sum(cg_iters) / args.steps,
                                 "bicgstab": sum(bi_iters) / args.steps},
-        "gpu_launches": int(launches),
+        "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,
     }
-    print(json.dumps(out))
+    if D.rank == 0:
+        print(json.dumps(out))
+    D.close()
 
 
 def main():

@@ -96,7 +96,22 @@ int fvb_upload_mesh(fvb_ctx* ctx, int64_t n_cells, int64_t n_faces,
                     const double* smag, const double* vol, const double* w,
                     const double* d, const double* db);
 
-/* Upload the hybrid pattern once (build_pattern, sparse.py:212-220). */
+/* Domain-decomposed variant: the local mesh of one rank
+ * holds n_rows owned cells followed by n_cells - n_rows ghost cells (cells
+ * of other ranks adjacent to an owned cell).  Faces are the local faces
+ * (every face with an owned side) in ascending global order, internal
+ * faces first; processor faces are internal faces with a ghost side.
+ * Only owned rows are assembled and solved; ghost values arrive by halo
+ * exchange.  fvb_upload_mesh(...) == fvb_upload_mesh_part(n_rows=n_cells). */
+int fvb_upload_mesh_part(fvb_ctx* ctx, int64_t n_cells, int64_t n_rows,
+                         int64_t n_faces, int64_t n_internal,
+                         const int64_t* owner, const int64_t* neighbour,
+                         const double* sf, const double* smag, const double* vol,
+                         const double* w, const double* d, const double* db);
+
+/* Upload the hybrid pattern once (build_pattern, sparse.py:212-220).
+ * n = owned rows; columns may address ghost cells (< n_cells); a negative
+ * face_addr entry marks a side whose row lives on another rank. */
 int fvb_upload_pattern(fvb_ctx* ctx, int64_t n, int64_t k, const int64_t* I,
                        const int64_t* diag_slot, const int64_t* face_addr,
                        int64_t n_face_pairs, int64_t nnz_crs,
@@ -227,6 +242,37 @@ int fvb_op_face_flux(fvb_ctx* ctx, const double* values, const double* boundary,
 int fvb_plain_flux(fvb_ctx* ctx);
 /* continuity_error (coupling.py:373-375) */
 int fvb_continuity_error(fvb_ctx* ctx, double* out);
+/* ------------------------------------------------------------- team
+ * Ranks of one domain decomposition share their cell pools: kernels store
+ * halo values straight into the neighbours' ghost slots (NVLink P2P) and
+ * combine reduction partials through peer mailboxes, inside the persistent
+ * Krylov kernels.  Across processes the pools travel as CUDA IPC handles
+ * (64 bytes, exchanged by the caller, e.g. torch.distributed); ranks in one
+ * process pass the raw pool pointers.  There is no reference counterpart:
+ * fvflow is single-process. */
+/* pool base (device pointer), local cell count and IPC handle of a context */
+int fvb_team_export(fvb_ctx* ctx, void** pool_base, int64_t* n_cells,
+                    uint8_t* ipc_handle /* 64 bytes */);
+int fvb_ipc_open(const uint8_t* ipc_handle, void** pool_base);
+int fvb_ipc_close(void* pool_base);
+/* attach this context as `rank` of `size`: pool_bases[q] / n_cells[q] of
+ * every rank (own included); owned rows >= n_inner send their values to
+ * (send_rank[e], ghost index send_dst[e]) for e in
+ * send_ptr[row-n_inner] .. send_ptr[row-n_inner+1] */
+int fvb_team_attach(fvb_ctx* ctx, int rank, int size, void* const* pool_bases,
+                    const int64_t* n_cells, int64_t n_inner,
+                    const int64_t* send_ptr, const int64_t* send_rank,
+                    const int64_t* send_dst);
+/* after every rank attached: make the mesh checks that raise inside a step
+ * (coincident centroids, fvm.py:349-370) raise on every rank (team sync) */
+int fvb_team_check(fvb_ctx* ctx);
+/* deterministic allreduce of m <= 16 doubles over the team (op 0 sum,
+ * 1 max, 2 min); a no-op without a team */
+int fvb_team_allreduce(fvb_ctx* ctx, double* vals, int m, int op);
+/* several teams sharing one device (tests): persistent grids use 1/share
+ * of the SMs so every rank's solver kernel is co-resident */
+int fvb_set_sm_share(fvb_ctx* ctx, int share);
+
 /* number of kernels libfvb has launched in this process (bench evidence) */
 unsigned long long fvb_launch_count(void);
 /* page-lock caller-owned host buffers (pinned H2D/D2H for the e2e path) */

@@ -130,7 +130,15 @@ _sig("fvb_ctx_create", I, I, C.POINTER(vp))
 _sig("fvb_ctx_destroy", I, vp)
 _sig("fvb_ctx_device_bytes", I64, vp)
 _sig("fvb_upload_mesh", I, vp, I64, I64, I64, i64p, i64p, dp, dp, dp, dp, dp, dp)
+_sig("fvb_upload_mesh_part", I, vp, I64, I64, I64, I64, i64p, i64p, dp, dp, dp, dp, dp, dp)
 _sig("fvb_upload_pattern", I, vp, I64, I64, i64p, i64p, i64p, I64, I64, i64p, i64p)
+_sig("fvb_team_export", I, vp, C.POINTER(vp), i64p, u8p)
+_sig("fvb_ipc_open", I, u8p, C.POINTER(vp))
+_sig("fvb_ipc_close", I, vp)
+_sig("fvb_team_attach", I, vp, I, I, C.POINTER(vp), i64p, I64, i64p, i64p, i64p)
+_sig("fvb_team_check", I, vp)
+_sig("fvb_team_allreduce", I, vp, dp, I, I)
+_sig("fvb_set_sm_share", I, vp, I)
 _sig("fvb_set_bcs", I, vp, I, u8p, i32p, dp, I)
 _sig("fvb_set_state", I, vp, dp, dp, dp, dp, dp)
 _sig("fvb_get_state", I, vp, dp, dp, dp, dp, dp)
@@ -163,6 +171,8 @@ EXPORTS = [
     "fvb_version", "fvb_last_error", "fvb_device_count", "fvb_geometry",
     "fvb_pattern_plan_create", "fvb_pattern_plan_fill", "fvb_pattern_plan_destroy",
     "fvb_ctx_create", "fvb_ctx_destroy", "fvb_ctx_device_bytes", "fvb_upload_mesh",
+    "fvb_upload_mesh_part", "fvb_team_export", "fvb_ipc_open", "fvb_ipc_close",
+    "fvb_team_attach", "fvb_team_check", "fvb_team_allreduce", "fvb_set_sm_share",
     "fvb_upload_pattern", "fvb_set_bcs", "fvb_set_state", "fvb_get_state", "fvb_op_smvp",
     "fvb_op_cg", "fvb_op_bicgstab", "fvb_op_bicgstab_batched", "fvb_op_apply_bcs",
     "fvb_op_interpolate", "fvb_op_gradient", "fvb_op_divergence", "fvb_op_laplacian",

@@ -11,7 +11,7 @@
 #include "fvb_internal.cuh"
 
 static thread_local std::string g_last_error;
-unsigned long long fvb::g_launches = 0;
+std::atomic<unsigned long long> fvb::g_launches{0};
 
 void fvb_set_error(const char* fmt, ...) {
   char buf[1024];
@@ -23,6 +23,34 @@ void fvb_set_error(const char* fmt, ...) {
 }
 
 using namespace fvb;
+
+namespace fvb {
+// One allocation: the team comm area followed by kPoolSlots cell vectors.
+// Without a team the context is its own rank 0 of size 1.
+int ensure_pool(Ctx* c) {
+  if (c->pool) return FVB_OK;
+  const size_t bytes = kCommBytes + sizeof(double) * size_t(kPoolSlots) * size_t(c->nc);
+  char* p = nullptr;
+  FVB_TRY(dalloc(c, &p, bytes));
+  FVB_CUDA(cudaMemset(p, 0, bytes));
+  c->pool = p;
+  c->cells = reinterpret_cast<double*>(p + kCommBytes);
+  c->u = c->slot(S_U);
+  c->p = c->slot(S_P);
+  c->scratch = c->slot(S_SCR);
+  TeamView& T = c->team;
+  T = TeamView{};
+  T.rank = 0;
+  T.size = 1;
+  T.comm = reinterpret_cast<Comm*>(p);
+  T.peer_comm[0] = T.comm;
+  T.peer_cells[0] = c->cells;
+  T.peer_nc[0] = c->nc;
+  T.n_inner = c->nr;
+  return FVB_OK;
+}
+}  // namespace fvb
+
 
 namespace {
 
@@ -87,7 +115,7 @@ struct DevMatrix {
 };
 
 int upload_matrix(Ctx* c, DevMatrix& M, const double* V, const double* crs) {
-  std::vector<double> sm = to_slot_major(V, c->nc, c->k);
+  std::vector<double> sm = to_slot_major(V, c->nr, c->k);
   double* dv;
   double* dc;
   FVB_TRY(tmp_upload(c, M.tv, sm.data(), sm.size(), &dv));
@@ -97,11 +125,11 @@ int upload_matrix(Ctx* c, DevMatrix& M, const double* V, const double* crs) {
 }
 
 int download_matrix(Ctx* c, DevMatrix& M, double* V, double* crs) {
-  std::vector<double> sm(size_t(c->nc) * c->k);
+  std::vector<double> sm(size_t(c->nr) * c->k);
   FVB_TRY(d2h(c, sm.data(), M.m.V, sm.size()));
   if (crs) FVB_TRY(d2h(c, crs, M.m.crs, size_t(c->nnz_crs)));
   FVB_TRY(sync(c));
-  from_slot_major(sm, V, c->nc, c->k);
+  from_slot_major(sm, V, c->nr, c->k);
   return FVB_OK;
 }
 
@@ -128,12 +156,8 @@ int need_bc(Ctx* c, int field) {
 }
 
 // ---------------------------------------------------------------- kernels
-__global__ void k_fill(double* a, size_t n, double v) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
-       i += size_t(gridDim.x) * blockDim.x)
-    a[i] = v;
-}
-
+// Row kernels loop over the nr owned rows; V has slot stride nr, cell
+// vectors have component stride nv (= nc, owned rows + ghosts).
 __global__ void k_get_diag(int n, const int* ds, const double* V, double* diag) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     diag[i] = V[size_t(ds[i]) * n + i];
@@ -146,9 +170,9 @@ __global__ void k_set_diag(int n, const int* ds, double* V, const double* diag) 
 
 // rhs = b0 - V grad p   (coupling.py:253); SIMPLE implicit relaxation
 // (coupling.py:254-258): V[diag] = diag/alpha, rhs += (scaled - diag) u
-__global__ void k_mom_rhs(int n, const double* b0, const double* vol, const double* gp,
-                          const double* diag, const double* u, double* rhs, double* V,
-                          const int* ds, int relax, double alpha_u) {
+__global__ void k_mom_rhs(int n, size_t nv, const double* b0, const double* vol,
+                          const double* gp, const double* diag, const double* u, double* rhs,
+                          double* V, const int* ds, int relax, double alpha_u) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double v = vol[i];
     double scaled = 0.0;
@@ -157,20 +181,20 @@ __global__ void k_mom_rhs(int n, const double* b0, const double* vol, const doub
       V[size_t(ds[i]) * n + i] = scaled;
     }
     for (int c = 0; c < 3; ++c) {
-      double r = b0[size_t(c) * n + i] - v * gp[size_t(c) * n + i];
-      if (relax) r = r + (scaled - diag[i]) * u[size_t(c) * n + i];
-      rhs[size_t(c) * n + i] = r;
+      double r = b0[c * nv + i] - v * gp[c * nv + i];
+      if (relax) r = r + (scaled - diag[i]) * u[c * nv + i];
+      rhs[c * nv + i] = r;
     }
   }
 }
 
-// per-block sum of squares of up to 3 arrays (partials, fixed order)
-__global__ void k_sumsq(int n, int ncomp, const double* x, double* partials) {
+// per-block sum of squares of up to 3 vectors (partials, fixed order)
+__global__ void k_sumsq(int n, size_t nv, int ncomp, const double* x, double* partials) {
   __shared__ double red[32 * 3];
   double acc[3] = {0.0, 0.0, 0.0};
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     for (int c = 0; c < ncomp; ++c) {
-      const double v = x[size_t(c) * n + i];
+      const double v = x[c * nv + i];
       acc[c] += v * v;
     }
   block_reduce<3>(acc, red);
@@ -194,12 +218,12 @@ __global__ void k_absmax(int n, const double* x, double* partials) {
 }
 
 // HbyA = u + (b0 - A u)/a_P  (coupling.py:290-291); rAU = V/a_P (301)
-__global__ void k_hbya(int n, const double* u, const double* b0, const double* au,
+__global__ void k_hbya(int n, size_t nv, const double* u, const double* b0, const double* au,
                        const double* diag, const double* vol, double* hv, double* rau) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double d = diag[i];
     for (int c = 0; c < 3; ++c) {
-      const size_t k = size_t(c) * n + i;
+      const size_t k = c * nv + i;
       hv[k] = u[k] + (b0[k] - au[k]) / d;
     }
     rau[i] = vol[i] / d;
@@ -230,20 +254,16 @@ __global__ void k_relax_p(int n, double* p, const double* pb, double a) {
 }
 
 // u = HbyA - rAU grad p  (coupling.py:341)
-__global__ void k_u_corr(int n, const double* hv, const double* rau, const double* gp, double* u) {
+__global__ void k_u_corr(int n, size_t nv, const double* hv, const double* rau, const double* gp,
+                         double* u) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    for (int c = 0; c < 3; ++c) u[size_t(c) * n + i] = hv[size_t(c) * n + i] - rau[i] * gp[size_t(c) * n + i];
+    for (int c = 0; c < 3; ++c) u[c * nv + i] = hv[c * nv + i] - rau[i] * gp[c * nv + i];
 }
 
-int fill(Ctx* c, double* a, size_t n, double v) {
-  { k_fill<<<grid_for(int64_t(n), kThreads), kThreads, 0, c->stream>>>(a, n, v); fvb::note_launch(); }
-  FVB_CUDA(cudaGetLastError());
-  return FVB_OK;
-}
-
+// ||x_c||^2 over the owned rows of the whole team (deterministic)
 int sumsq(Ctx* c, int ncomp, const double* x, double* out) {
   const int blocks = 2 * c->num_sms;
-  { k_sumsq<<<blocks, kThreads, 0, c->stream>>>(c->nc, ncomp, x, c->partials); fvb::note_launch(); }
+  { k_sumsq<<<blocks, kThreads, 0, c->stream>>>(c->nr, size_t(c->nc), ncomp, x, c->partials); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   std::vector<double> h(3 * size_t(blocks));
   FVB_TRY(d2h(c, h.data(), c->partials, h.size()));
@@ -253,67 +273,38 @@ int sumsq(Ctx* c, int ncomp, const double* x, double* out) {
     for (int b = 0; b < blocks; ++b) s += h[size_t(k) * blocks + b];
     out[k] = s;
   }
-  return FVB_OK;
+  return team_allreduce(c, out, ncomp, RED_SUM);
 }
 
 // ----------------------------------------------------------- step state
+// Cell vectors of the step live in pool slots (Slot enum); matrices and
+// face arrays are plain allocations owned by the context.
 struct StepWork {
-  bool ready = false;
-  double *Vm, *crsm, *b0, *diag, *rhs, *gu, *gp, *hv, *au, *phih, *divh, *rau, *rauf, *Vp, *crsp,
-      *rl, *rp, *coef, *corr, *lf, *pbefore;
+  double*& Vm; double*& crsm; double*& Vp; double*& crsp; double*& phih; double*& rauf;
+  double*& coef; double*& corr; double*& lf;
 };
 
-StepWork& work_of(Ctx* c);
+StepWork work_of(Ctx* c) {
+  return StepWork{c->Vm, c->crsm, c->Vp, c->crsp, c->phih, c->rauf, c->coef, c->corr, c->lf};
+}
 
 int ensure_work(Ctx* c) {
-  StepWork& w = work_of(c);
-  if (w.ready) return FVB_OK;
-  const size_t n = c->nc, nf = c->nf, kn = size_t(c->k) * n, nz = size_t(c->nnz_crs);
-  FVB_TRY(dalloc(c, &w.Vm, kn));
-  FVB_TRY(dalloc(c, &w.crsm, nz));
-  FVB_TRY(dalloc(c, &w.b0, 3 * n));
-  FVB_TRY(dalloc(c, &w.diag, n));
-  FVB_TRY(dalloc(c, &w.rhs, 3 * n));
-  FVB_TRY(dalloc(c, &w.gu, 9 * n));
-  FVB_TRY(dalloc(c, &w.gp, 3 * n));
-  FVB_TRY(dalloc(c, &w.hv, 3 * n));
-  FVB_TRY(dalloc(c, &w.au, 3 * n));
-  FVB_TRY(dalloc(c, &w.phih, nf));
-  FVB_TRY(dalloc(c, &w.divh, n));
-  FVB_TRY(dalloc(c, &w.rau, n));
-  FVB_TRY(dalloc(c, &w.rauf, nf));
-  FVB_TRY(dalloc(c, &w.Vp, kn));
-  FVB_TRY(dalloc(c, &w.crsp, nz));
-  FVB_TRY(dalloc(c, &w.rl, n));
-  FVB_TRY(dalloc(c, &w.rp, n));
-  FVB_TRY(dalloc(c, &w.coef, nf));
-  FVB_TRY(dalloc(c, &w.corr, nf));
-  FVB_TRY(dalloc(c, &w.lf, nf));
-  FVB_TRY(dalloc(c, &w.pbefore, n));
-  w.ready = true;
+  if (c->work_ready || !c->have_mesh || !c->have_pattern) return FVB_OK;
+  const size_t nf = c->nf, kn = size_t(c->k) * c->nr, nz = size_t(c->nnz_crs);
+  FVB_TRY(dalloc(c, &c->Vm, kn));
+  FVB_TRY(dalloc(c, &c->crsm, nz));
+  FVB_TRY(dalloc(c, &c->Vp, kn));
+  FVB_TRY(dalloc(c, &c->crsp, nz));
+  FVB_TRY(dalloc(c, &c->phih, nf));
+  FVB_TRY(dalloc(c, &c->rauf, nf));
+  FVB_TRY(dalloc(c, &c->coef, nf));
+  FVB_TRY(dalloc(c, &c->corr, nf));
+  FVB_TRY(dalloc(c, &c->lf, nf));
+  c->work_ready = true;
   return FVB_OK;
 }
 
-struct CtxExt {
-  StepWork work;
-};
-std::vector<std::pair<Ctx*, CtxExt*>> g_ext;
-
-StepWork& work_of(Ctx* c) {
-  for (auto& e : g_ext)
-    if (e.first == c) return e.second->work;
-  g_ext.push_back({c, new CtxExt()});
-  return g_ext.back().second->work;
-}
-
-void drop_ext(Ctx* c) {
-  for (size_t i = 0; i < g_ext.size(); ++i)
-    if (g_ext[i].first == c) {
-      delete g_ext[i].second;
-      g_ext.erase(g_ext.begin() + i);
-      return;
-    }
-}
+void drop_ext(Ctx*) {}
 
 void fill_report(fvb_solve_report& r, const SolveOut& o) {
   r.iterations = o.iterations;
@@ -345,34 +336,43 @@ float ev_ms(Ctx* c, int a, int b) {
 
 // _momentum_matrix (coupling.py:216-231)
 int momentum_matrix(Ctx* c, const fvb_step_cfg* cfg, bool with_ddt) {
-  StepWork& w = work_of(c);
-  const size_t n = c->nc;
+  StepWork w = work_of(c);
+  const size_t n = c->nr;
+  double* b0 = c->slot(S_B0);
+  double* gu = c->slot(S_GU);
   MatView Am{w.Vm, w.crsm};
   FVB_CUDA(cudaMemsetAsync(w.Vm, 0, sizeof(double) * c->k * n, c->stream));
   if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsm, 0, sizeof(double) * c->nnz_crs, c->stream));
-  FVB_CUDA(cudaMemsetAsync(w.b0, 0, sizeof(double) * 3 * n, c->stream));
-  if (with_ddt) FVB_TRY(op_ddt(c, 3, Am, w.b0, c->u, cfg->dt, 1.0));
-  FVB_TRY(op_convection(c, 0, 3, Am, w.b0, c->flux, c->ub, cfg->scheme, 1.0));
+  FVB_CUDA(cudaMemsetAsync(b0, 0, sizeof(double) * 3 * size_t(c->nc), c->stream));
+  if (with_ddt) FVB_TRY(op_ddt(c, 3, Am, b0, c->u, cfg->dt, 1.0));
+  FVB_TRY(op_convection(c, 0, 3, Am, b0, c->flux, c->ub, cfg->scheme, 1.0));
   const bool corr = cfg->nonorth_correction && cfg->limiter > 0.0;
-  if (corr) FVB_TRY(op_gradient(c, 0, 3, c->u, c->ub, w.gu));
-  FVB_TRY(op_laplacian(c, 0, 3, Am, w.b0, cfg->nu, nullptr, c->u, c->ub, w.gu,
+  if (corr) {
+    FVB_TRY(op_gradient(c, 0, 3, c->u, c->ub, gu));
+    FVB_TRY(team_halo(c, S_GU, 9));  // face-interpolated gradient on processor faces
+  }
+  FVB_TRY(op_laplacian(c, 0, 3, Am, b0, cfg->nu, nullptr, c->u, c->ub, gu,
                        cfg->nonorth_correction, cfg->limiter, -1.0, nullptr, nullptr));
   return FVB_OK;
 }
 
 // _solve_momentum (coupling.py:234-279); returns worst normalised residual
 int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report* rep) {
-  StepWork& w = work_of(c);
-  const int n = c->nc;
+  StepWork w = work_of(c);
+  const int n = c->nr;
+  const size_t nv = c->nc;
   const int g = grid_for(n, kThreads);
-  { k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag); fvb::note_launch(); }
-  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
+  double* diag = c->slot(S_DIAG);
+  double* gp = c->slot(S_GP);
+  double* rhs = c->slot(S_RHS);
+  { k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, diag); fvb::note_launch(); }
+  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
   const bool relaxing = relax && cfg->alpha_u < 1.0;
-  { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, w.b0, c->vol, w.gp, w.diag, c->u, w.rhs, w.Vm,
-                                           c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
+  { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, nv, c->slot(S_B0), c->vol, gp, diag, c->u, rhs,
+                                           w.Vm, c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   double bn2[3];
-  FVB_TRY(sumsq(c, 3, w.rhs, bn2));
+  FVB_TRY(sumsq(c, 3, rhs, bn2));
   double bn[3], bscale = 0.0;
   for (int k = 0; k < 3; ++k) {
     bn[k] = std::sqrt(bn2[k]);
@@ -380,8 +380,8 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   }
   bscale = std::max(bscale, 1e-30);
   FVB_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  const double* b[3] = {w.rhs, w.rhs + n, w.rhs + 2 * size_t(n)};
-  double* x[3] = {c->u, c->u + n, c->u + 2 * size_t(n)};
+  const double* b[3] = {rhs, rhs + nv, rhs + 2 * nv};
+  double* x[3] = {c->u, c->u + nv, c->u + 2 * nv};
   SolveOut out[3];
   FVB_TRY(bicgstab_solve(c, MatView{w.Vm, w.crsm}, 3, b, x, cfg->mom_tol, cfg->mom_abs_tol,
                          cfg->mom_max_iters, out));
@@ -399,9 +399,10 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
     worst = std::max(worst, out[k].res0 * bn[k] / bscale);
   }
   if (relaxing) {
-    { k_set_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, w.diag); fvb::note_launch(); }
+    { k_set_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, diag); fvb::note_launch(); }
     FVB_CUDA(cudaGetLastError());
   }
+  FVB_TRY(team_halo(c, S_U, 3));  // A u of the correctors gathers ghost u
   rep->mom_res = worst;
   return FVB_OK;
 }
@@ -409,18 +410,29 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
 // _pressure_correct (coupling.py:282-344)
 int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_report* rep,
                      double* first_res, double* t_asm, double* t_solve, double* t_corr) {
-  StepWork& w = work_of(c);
-  const int n = c->nc;
+  StepWork w = work_of(c);
+  const int n = c->nr;
+  const size_t nv = c->nc;
   const int g = grid_for(n, kThreads);
+  double* hv = c->slot(S_HV);
+  double* rau = c->slot(S_RAU);
+  double* au = c->slot(S_AU);
+  double* gp = c->slot(S_GP);
+  double* divh = c->slot(S_DIVH);
+  double* rl = c->slot(S_RL);
+  double* rp = c->slot(S_RP);
+  double* pbefore = c->slot(S_PBEFORE);
   FVB_CUDA(cudaEventRecord(c->ev[4], c->stream));
   MatView Am{w.Vm, w.crsm};
-  for (int k = 0; k < 3; ++k) FVB_TRY(smvp(c, Am, c->u + size_t(k) * n, w.au + size_t(k) * n));
-  { k_hbya<<<g, kThreads, 0, c->stream>>>(n, c->u, w.b0, w.au, w.diag, c->vol, w.hv, w.rau); fvb::note_launch(); }
+  for (int k = 0; k < 3; ++k) FVB_TRY(smvp(c, Am, c->u + k * nv, au + k * nv));
+  { k_hbya<<<g, kThreads, 0, c->stream>>>(n, nv, c->u, c->slot(S_B0), au, c->slot(S_DIAG), c->vol,
+                                        hv, rau); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
-  FVB_TRY(op_face_flux(c, 3, w.hv, c->ub, 0, w.phih));
-  FVB_TRY(op_divergence(c, w.phih, w.divh));
-  FVB_TRY(op_interp(c, -1, 1, w.rau, nullptr, w.rauf));
-  if (relax_p) FVB_CUDA(cudaMemcpyAsync(w.pbefore, c->p, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  FVB_TRY(team_halo(c, S_HV, 4));  // HbyA and rAU on processor faces
+  FVB_TRY(op_face_flux(c, 3, hv, c->ub, 0, w.phih));
+  FVB_TRY(op_divergence(c, w.phih, divh));
+  FVB_TRY(op_interp(c, -1, 1, rau, nullptr, w.rauf));
+  if (relax_p) FVB_CUDA(cudaMemcpyAsync(pbefore, c->p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c->stream));
   FVB_CUDA(cudaEventRecord(c->ev[5], c->stream));
   float asm_ms = 0.f, solve_ms = 0.f;
   const bool corr = cfg->nonorth_correction && cfg->limiter > 0.0;
@@ -429,18 +441,21 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
     FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
     FVB_CUDA(cudaMemsetAsync(w.Vp, 0, sizeof(double) * c->k * size_t(n), c->stream));
     if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsp, 0, sizeof(double) * c->nnz_crs, c->stream));
-    FVB_CUDA(cudaMemsetAsync(w.rl, 0, sizeof(double) * n, c->stream));
-    if (corr) FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
-    FVB_TRY(op_laplacian(c, 1, 1, Ap, w.rl, 0.0, w.rauf, c->p, c->pb, w.gp,
+    FVB_CUDA(cudaMemsetAsync(rl, 0, sizeof(double) * nv, c->stream));
+    if (corr) {
+      FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+      FVB_TRY(team_halo(c, S_GP, 3));
+    }
+    FVB_TRY(op_laplacian(c, 1, 1, Ap, rl, 0.0, w.rauf, c->p, c->pb, gp,
                          cfg->nonorth_correction, cfg->limiter, -1.0, w.coef, w.corr));
-    { k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, w.rl, w.divh, w.rp); fvb::note_launch(); }
+    { k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, rl, divh, rp); fvb::note_launch(); }
     if (cfg->pin_pressure)
-      { k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, w.rp, cfg->pressure_ref_cell,
+      { k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, rp, cfg->pressure_ref_cell,
                                     cfg->pressure_ref_value); fvb::note_launch(); }
     FVB_CUDA(cudaGetLastError());
     FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
     SolveOut o;
-    FVB_TRY(cg_solve(c, Ap, w.rp, c->p, cfg->p_tol, cfg->p_abs_tol, cfg->p_max_iters, &o));
+    FVB_TRY(cg_solve(c, Ap, rp, c->p, cfg->p_tol, cfg->p_abs_tol, cfg->p_max_iters, &o));
     asm_ms += ev_ms(c, 6, 7);
     FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
     FVB_CUDA(cudaEventSynchronize(c->ev[6]));
@@ -453,17 +468,24 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
     }
     FVB_TRY(log_solve(rep, 0, 3, o));
     if (*first_res < 0) *first_res = o.res0;
+    FVB_TRY(team_halo(c, S_P, 1));  // unrelaxed p on processor faces
   }
   FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
   FVB_TRY(op_lap_flux(c, 1, 1, w.coef, w.corr, c->p, c->pb, w.lf));
   { k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux); fvb::note_launch(); }
-  if (relax_p && cfg->alpha_p < 1.0)
-    { k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, w.pbefore, cfg->alpha_p); fvb::note_launch(); }
+  if (relax_p && cfg->alpha_p < 1.0) {
+    // the neighbours may still be reading the unrelaxed ghost p (their
+    // laplacian_face_flux): sync before overwriting it (write-after-read)
+    FVB_TRY(team_halo(c, S_P, 0));
+    { k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, pbefore, cfg->alpha_p); fvb::note_launch(); }
+    FVB_TRY(team_halo(c, S_P, 1));
+  }
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
-  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, w.gp));
-  { k_u_corr<<<g, kThreads, 0, c->stream>>>(n, w.hv, w.rau, w.gp, c->u); fvb::note_launch(); }
+  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+  { k_u_corr<<<g, kThreads, 0, c->stream>>>(n, nv, hv, rau, gp, c->u); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
+  FVB_TRY(team_halo(c, S_U, 3));
   FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
   FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
   FVB_CUDA(cudaEventSynchronize(c->ev[7]));
@@ -502,6 +524,15 @@ int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_rep
     FVB_TRY(pressure_correct(c, cfg, !piso, rep, &first, &rep->t_pressure_assembly,
                              &rep->t_pressure_solve, &rep->t_correction));
   rep->p_res = first;
+  if (c->teamed()) {
+    unsigned err = 0;
+    FVB_CUDA(cudaMemcpyAsync(&err, c->sync + 3, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+    FVB_CUDA(cudaStreamSynchronize(c->stream));
+    if (err) {
+      fvb_set_error("team sync timed out during the step (rank %d)", c->team.rank);
+      return FVB_E_TIMEOUT;
+    }
+  }
   return FVB_OK;
 }
 
@@ -569,26 +600,31 @@ int fvb_ctx_destroy(fvb_ctx* h) {
 
 int64_t fvb_ctx_device_bytes(fvb_ctx* h) { return h ? h->c.bytes : 0; }
 
-int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_internal,
-                    const int64_t* owner, const int64_t* neighbour, const double* sf,
-                    const double* smag, const double* vol, const double* w, const double* d,
-                    const double* db) {
+int fvb_upload_mesh_part(fvb_ctx* h, int64_t n_cells, int64_t n_rows, int64_t n_faces,
+                         int64_t n_internal, const int64_t* owner, const int64_t* neighbour,
+                         const double* sf, const double* smag, const double* vol, const double* w,
+                         const double* d, const double* db) {
   Ctx* c = &h->c;
   cudaSetDevice(c->dev);
   if (c->have_mesh) {
     fvb_set_error("mesh already uploaded");
     return FVB_E_ARG;
   }
-  if (n_cells <= 0 || n_faces < n_internal || n_faces >= (int64_t(1) << 31) ||
-      n_cells >= (int64_t(1) << 31)) {
+  if (n_cells <= 0 || n_rows <= 0 || n_rows > n_cells || n_faces < n_internal ||
+      n_faces >= (int64_t(1) << 31) || n_cells >= (int64_t(1) << 31)) {
     fvb_set_error("mesh sizes out of range");
     return FVB_E_ARG;
   }
+  if (c->have_pattern && n_rows != c->nr) {
+    fvb_set_error("mesh rows %lld do not match the pattern rows %d", (long long)n_rows, c->nr);
+    return FVB_E_MESH;
+  }
   c->nc = int(n_cells);
+  c->nr = int(n_rows);
   c->nf = int(n_faces);
   c->ni = int(n_internal);
   c->nb = c->nf - c->ni;
-  const size_t nc = c->nc, nf = c->nf, ni = c->ni, nb = c->nb;
+  const size_t nc = c->nc, nr = c->nr, nf = c->nf, ni = c->ni, nb = c->nb;
   std::vector<int> own(nf), nbr(ni);
   for (size_t f = 0; f < nf; ++f) {
     if (owner[f] < 0 || owner[f] >= n_cells) {
@@ -604,12 +640,20 @@ int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_inte
     }
     nbr[f] = int(neighbour[f]);
   }
-  // per-cell face list: owned faces ascending, then neighbour faces ascending
-  std::vector<int> nown(nc, 0), nnb(nc, 0);
-  for (size_t f = 0; f < nf; ++f) nown[own[f]]++;
-  for (size_t f = 0; f < ni; ++f) nnb[nbr[f]]++;
-  std::vector<int> ptr(nc + 1, 0);
-  for (size_t i = 0; i < nc; ++i) {
+  for (size_t f = ni; f < nf; ++f)
+    if (size_t(own[f]) >= nr) {
+      fvb_set_error("boundary face %zu is owned by a ghost cell", f);
+      return FVB_E_MESH;
+    }
+  // per-row face list: owned faces ascending, then neighbour faces ascending
+  // (ghost cells get no list: their rows belong to another rank)
+  std::vector<int> nown(nr, 0), nnb(nr, 0);
+  for (size_t f = 0; f < nf; ++f)
+    if (size_t(own[f]) < nr) nown[own[f]]++;
+  for (size_t f = 0; f < ni; ++f)
+    if (size_t(nbr[f]) < nr) nnb[nbr[f]]++;
+  std::vector<int> ptr(nr + 1, 0);
+  for (size_t i = 0; i < nr; ++i) {
     const int64_t next = int64_t(ptr[i]) + nown[i] + nnb[i];
     if (next >= (int64_t(1) << 31)) {
       fvb_set_error("face list too long");
@@ -617,14 +661,16 @@ int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_inte
     }
     ptr[i + 1] = int(next);
   }
-  std::vector<int> cf(ptr[nc]);
-  std::vector<int> po(nc), pn(nc);
-  for (size_t i = 0; i < nc; ++i) {
+  std::vector<int> cf(ptr[nr]);
+  std::vector<int> po(nr), pn(nr);
+  for (size_t i = 0; i < nr; ++i) {
     po[i] = ptr[i];
     pn[i] = ptr[i] + nown[i];
   }
-  for (size_t f = 0; f < nf; ++f) cf[po[own[f]]++] = int(f);
-  for (size_t f = 0; f < ni; ++f) cf[pn[nbr[f]]++] = ~int(f);
+  for (size_t f = 0; f < nf; ++f)
+    if (size_t(own[f]) < nr) cf[po[own[f]]++] = int(f);
+  for (size_t f = 0; f < ni; ++f)
+    if (size_t(nbr[f]) < nr) cf[pn[nbr[f]]++] = ~int(f);
   // SoA geometry
   std::vector<double> tmp(std::max(nf, nc));
   auto up3 = [&](const double* src, size_t m, double** o0, double** o1, double** o2) -> int {
@@ -632,7 +678,7 @@ int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_inte
     for (int k = 0; k < 3; ++k) {
       FVB_TRY(dalloc(c, &outs[k], m));
       for (size_t i = 0; i < m; ++i) tmp[i] = src[3 * i + k];
-      FVB_CUDA(cudaMemcpy(outs[k], tmp.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+      if (m) FVB_CUDA(cudaMemcpy(outs[k], tmp.data(), m * sizeof(double), cudaMemcpyHostToDevice));
     }
     *o0 = outs[0];
     *o1 = outs[1];
@@ -641,12 +687,12 @@ int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_inte
   };
   auto up1 = [&](const auto* src, size_t m, auto** o) -> int {
     FVB_TRY(dalloc(c, o, m));
-    FVB_CUDA(cudaMemcpy(*o, src, m * sizeof(**o), cudaMemcpyHostToDevice));
+    if (m) FVB_CUDA(cudaMemcpy(*o, src, m * sizeof(**o), cudaMemcpyHostToDevice));
     return FVB_OK;
   };
   FVB_TRY(up1(own.data(), nf, &c->own));
   FVB_TRY(up1(nbr.data(), ni, &c->nbr));
-  FVB_TRY(up1(ptr.data(), nc + 1, &c->cf_ptr));
+  FVB_TRY(up1(ptr.data(), nr + 1, &c->cf_ptr));
   FVB_TRY(up1(cf.data(), cf.size(), &c->cf));
   FVB_TRY(up3(sf, nf, &c->sx, &c->sy, &c->sz));
   FVB_TRY(up1(smag, nf, &c->smag));
@@ -674,22 +720,27 @@ int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_inte
   for (size_t j = 0; j < nb; ++j)
     c->dbmag_host[j] = std::sqrt((db[3 * j] * db[3 * j] + db[3 * j + 1] * db[3 * j + 1]) +
                                  db[3 * j + 2] * db[3 * j + 2]);
-  // coupled state
-  FVB_TRY(dalloc(c, &c->u, 3 * nc));
-  FVB_TRY(dalloc(c, &c->p, nc));
+  // coupled state: u, p in the cell pool; face / boundary arrays apart
+  FVB_TRY(ensure_pool(c));
   FVB_TRY(dalloc(c, &c->flux, nf));
   FVB_TRY(dalloc(c, &c->ub, 3 * nb));
   FVB_TRY(dalloc(c, &c->pb, nb));
-  FVB_CUDA(cudaMemset(c->u, 0, 3 * nc * sizeof(double)));
-  FVB_CUDA(cudaMemset(c->p, 0, nc * sizeof(double)));
-  FVB_CUDA(cudaMemset(c->flux, 0, nf * sizeof(double)));
+  FVB_CUDA(cudaMemset(c->flux, 0, (nf ? nf : 1) * sizeof(double)));
   FVB_CUDA(cudaMemset(c->ub, 0, 3 * (nb ? nb : 1) * sizeof(double)));
   FVB_CUDA(cudaMemset(c->pb, 0, (nb ? nb : 1) * sizeof(double)));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
-  FVB_CUDA(cudaDeviceSynchronize());
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
   // the temporaries dx.. stay in the allocation list (freed with the context)
   c->have_mesh = true;
-  return FVB_OK;
+  return ensure_work(c);
+}
+
+int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_internal,
+                    const int64_t* owner, const int64_t* neighbour, const double* sf,
+                    const double* smag, const double* vol, const double* w, const double* d,
+                    const double* db) {
+  return fvb_upload_mesh_part(h, n_cells, n_cells, n_faces, n_internal, owner, neighbour, sf,
+                              smag, vol, w, d, db);
 }
 
 int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
@@ -701,8 +752,8 @@ int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
     fvb_set_error("pattern already uploaded");
     return FVB_E_ARG;
   }
-  if (c->have_mesh && n != c->nc) {
-    fvb_set_error("pattern size %lld does not match mesh cells %d", (long long)n, c->nc);
+  if (c->have_mesh && n != c->nr) {
+    fvb_set_error("pattern size %lld does not match mesh rows %d", (long long)n, c->nr);
     return FVB_E_SPARSE;
   }
   if (k < 1 || k > kMaxK) {
@@ -713,14 +764,21 @@ int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
     fvb_set_error("pattern too large");
     return FVB_E_SPARSE;
   }
-  if (!c->have_mesh) c->nc = int(n);
+  if (!c->have_mesh) c->nc = c->nr = int(n);
   c->k = int(k);
   c->nnz_crs = int(nnz_crs);
   const size_t nn = size_t(n), kk = size_t(k), nk = nn * kk;
   std::vector<int> Is(nk), sf(nk, -1), ds(nn);
   for (size_t i = 0; i < nn; ++i) {
     ds[i] = int(diag_slot[i]);
-    for (size_t s = 0; s < kk; ++s) Is[s * nn + i] = int(I[i * kk + s]);
+    for (size_t s = 0; s < kk; ++s) {
+      const int64_t col = I[i * kk + s];
+      if (col >= c->nc) {
+        fvb_set_error("pattern column %lld outside the %d local cells", (long long)col, c->nc);
+        return FVB_E_SPARSE;
+      }
+      Is[s * nn + i] = int(col);
+    }
   }
   std::vector<int> cptr(nn + 1, 0), ccol(nnz_crs), cface(nnz_crs, -1);
   if (nnz_crs) {
@@ -736,6 +794,7 @@ int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
     for (int64_t f = 0; f < n_face_pairs; ++f) {
       for (int side = 0; side < 2; ++side) {
         const int64_t a = face_addr[2 * f + side];
+        if (a < 0) continue;  // the row of that side belongs to another rank
         int* slot;
         if (a < split) {
           slot = &sf[size_t(a % k) * nn + size_t(a / k)];
@@ -764,11 +823,9 @@ int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
     FVB_TRY(up(ccol, &c->crs_col));
     FVB_TRY(up(cface, &c->crs_face));
   }
-  // solver scratch: BiCGStab x3 needs 1 + 8*3 vectors
-  c->scratch_n = 26 * nn;
-  FVB_TRY(dalloc(c, &c->scratch, c->scratch_n));
+  FVB_TRY(ensure_pool(c));
   c->have_pattern = true;
-  return FVB_OK;
+  return ensure_work(c);
 }
 
 int fvb_set_bcs(fvb_ctx* h, int field, const uint8_t* kind, const int32_t* patch,
@@ -1106,21 +1163,145 @@ int fvb_continuity_error(fvb_ctx* h, double* out) {
   Ctx* c = &h->c;
   cudaSetDevice(c->dev);
   FVB_TRY(need_mesh(c));
-  double* div = c->scratch;
-  if (!div) {
-    FVB_TRY(dalloc(c, &c->scratch, size_t(c->nc)));
-    div = c->scratch;
-  }
+  double* div = c->slot(S_SCR);
   FVB_TRY(op_divergence(c, c->flux, div));
   const int blocks = 2 * c->num_sms;
-  { k_absmax<<<blocks, kThreads, 0, c->stream>>>(c->nc, div, c->partials); fvb::note_launch(); }
+  { k_absmax<<<blocks, kThreads, 0, c->stream>>>(c->nr, div, c->partials); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   std::vector<double> hm(blocks);
   FVB_TRY(d2h(c, hm.data(), c->partials, size_t(blocks)));
   FVB_TRY(sync(c));
   double m = 0.0;
   for (double v : hm) m = std::max(m, v);
+  FVB_TRY(team_allreduce(c, &m, 1, RED_MAX));
   *out = m;
+  return FVB_OK;
+}
+
+// ------------------------------------------------------------------ team
+int fvb_team_export(fvb_ctx* h, void** pool_base, int64_t* n_cells, uint8_t* ipc_handle) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  if (!c->pool) {
+    fvb_set_error("team export needs an uploaded mesh");
+    return FVB_E_ARG;
+  }
+  if (pool_base) *pool_base = c->pool;
+  if (n_cells) *n_cells = c->nc;
+  if (ipc_handle) {
+    cudaIpcMemHandle_t hd;
+    FVB_CUDA(cudaIpcGetMemHandle(&hd, c->pool));
+    memcpy(ipc_handle, &hd, sizeof hd);
+  }
+  return FVB_OK;
+}
+
+int fvb_ipc_open(const uint8_t* ipc_handle, void** base) {
+  cudaIpcMemHandle_t hd;
+  memcpy(&hd, ipc_handle, sizeof hd);
+  FVB_CUDA(cudaIpcOpenMemHandle(base, hd, cudaIpcMemLazyEnablePeerAccess));
+  return FVB_OK;
+}
+
+int fvb_ipc_close(void* base) {
+  FVB_CUDA(cudaIpcCloseMemHandle(base));
+  return FVB_OK;
+}
+
+int fvb_team_attach(fvb_ctx* h, int rank, int size, void* const* pool_bases,
+                    const int64_t* n_cells, int64_t n_inner, const int64_t* send_ptr,
+                    const int64_t* send_rank, const int64_t* send_dst) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  if (!c->pool || !c->have_mesh) {
+    fvb_set_error("team attach needs an uploaded mesh");
+    return FVB_E_ARG;
+  }
+  if (size < 1 || size > kMaxTeam || rank < 0 || rank >= size) {
+    fvb_set_error("team rank %d of size %d outside 1..%d", rank, size, kMaxTeam);
+    return FVB_E_ARG;
+  }
+  if (n_inner < 0 || n_inner > c->nr) {
+    fvb_set_error("n_inner %lld outside 0..%d", (long long)n_inner, c->nr);
+    return FVB_E_ARG;
+  }
+  if (pool_bases[rank] != c->pool) {
+    fvb_set_error("pool_bases[rank] is not this context's pool");
+    return FVB_E_ARG;
+  }
+  TeamView& T = c->team;
+  T.rank = rank;
+  T.size = size;
+  T.comm = reinterpret_cast<Comm*>(c->pool);
+  for (int q = 0; q < kMaxTeam; ++q) {
+    T.peer_comm[q] = nullptr;
+    T.peer_cells[q] = nullptr;
+    T.peer_nc[q] = 0;
+  }
+  for (int q = 0; q < size; ++q) {
+    char* b = static_cast<char*>(pool_bases[q]);
+    T.peer_comm[q] = reinterpret_cast<Comm*>(b);
+    T.peer_cells[q] = reinterpret_cast<double*>(b + kCommBytes);
+    T.peer_nc[q] = int(n_cells[q]);
+  }
+  T.n_inner = int(n_inner);
+  const int nsr = c->nr - int(n_inner);
+  const int64_t ns = nsr > 0 ? send_ptr[nsr] : 0;
+  std::vector<int> sp(size_t(nsr) + 1), sr(static_cast<size_t>(ns)), sd(static_cast<size_t>(ns));
+  for (int t = 0; t <= nsr; ++t) sp[t] = int(send_ptr[t]);
+  for (int64_t e = 0; e < ns; ++e) {
+    if (send_rank[e] < 0 || send_rank[e] >= size || send_rank[e] == rank ||
+        send_dst[e] < 0 || send_dst[e] >= n_cells[send_rank[e]]) {
+      fvb_set_error("halo send %lld targets rank %lld cell %lld", (long long)e,
+                    (long long)send_rank[e], (long long)send_dst[e]);
+      return FVB_E_ARG;
+    }
+    sr[e] = int(send_rank[e]);
+    sd[e] = int(send_dst[e]);
+  }
+  auto up = [&](const std::vector<int>& v, int** o) -> int {
+    FVB_TRY(dalloc(c, o, v.size()));
+    if (!v.empty()) FVB_CUDA(cudaMemcpy(*o, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return FVB_OK;
+  };
+  FVB_TRY(up(sp, &c->send_ptr));
+  FVB_TRY(up(sr, &c->send_rank));
+  FVB_TRY(up(sd, &c->send_dst));
+  T.send_ptr = c->send_ptr;
+  T.send_rank = c->send_rank;
+  T.send_dst = c->send_dst;
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  // No team sync here: allocations and copies above must not overlap a
+  // peer's spinning sync kernel.  fvb_team_check (called by every rank
+  // after all ranks attached) makes the mesh checks team-consistent.
+  return FVB_OK;
+}
+
+int fvb_team_check(fvb_ctx* h) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  // mesh checks that raise inside a step must raise on every rank
+  double flags[3] = {double(c->first_zero_dmag >= 0), double(c->first_zero_dbmag_value[0] >= 0),
+                     double(c->first_zero_dbmag_value[1] >= 0)};
+  FVB_TRY(team_allreduce(c, flags, 3, RED_MAX));
+  if (flags[0] > 0 && c->first_zero_dmag < 0) c->first_zero_dmag = 0x7ffffffe;
+  for (int f = 0; f < 2; ++f)
+    if (flags[1 + f] > 0 && c->first_zero_dbmag_value[f] < 0) c->first_zero_dbmag_value[f] = 0x7ffffffe;
+  return FVB_OK;
+}
+
+int fvb_team_allreduce(fvb_ctx* h, double* vals, int m, int op) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  return team_allreduce(c, vals, m, op);
+}
+
+int fvb_set_sm_share(fvb_ctx* h, int share) {
+  if (share < 1) {
+    fvb_set_error("sm share must be >= 1");
+    return FVB_E_ARG;
+  }
+  h->c.sm_share = share;
   return FVB_OK;
 }
 
@@ -1138,7 +1319,7 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
   return run_step(c, cfg, u_speeds, rep, false);
 }
 
-unsigned long long fvb_launch_count(void) { return g_launches; }
+unsigned long long fvb_launch_count(void) { return g_launches.load(); }
 
 int fvb_host_register(void* ptr, int64_t bytes) {
   if (!ptr || bytes <= 0) return FVB_OK;

@@ -1,11 +1,17 @@
-// libfvb internals: device-resident mesh/pattern/state, shared kernels'
-// helpers, deterministic reductions and the grid barrier used by the
-// persistent Krylov kernels.  FP64 throughout; compiled with -fmad=false so
-// every a*b+c rounds twice, exactly like the numpy reference.
+// libfvb internals: device-resident mesh/pattern/state, shared kernel
+// helpers, deterministic reductions, and the team (domain-decomposition)
+// layer: every cell vector lives in one per-context "cell pool" whose
+// base address is shared with the other ranks of the team (CUDA IPC across
+// processes, plain pointers inside one process), so kernels store halo
+// values straight into a neighbour's ghost slots over NVLink and exchange
+// reduction partials through peer mailboxes.  FP64 throughout; compiled
+// with -fmad=false so every a*b+c rounds twice, exactly like the numpy
+// reference.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -31,16 +37,81 @@
 namespace fvb {
 
 constexpr int kMaxK = 1 << 20;  // K is a runtime bound on the generic path
+constexpr int kMaxTeam = 8;     // ranks of one domain decomposition (one node)
+constexpr int kMailM = 16;      // doubles per mailbox message
 
-// host-side count of kernel launches issued by libfvb (fvb_launch_count)
-extern unsigned long long g_launches;
-inline void note_launch() { ++g_launches; }
+// host-side count of kernel launches issued by libfvb (fvb_launch_count);
+// ranks of an in-process team launch from several host threads
+extern std::atomic<unsigned long long> g_launches;
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ------------------------------------------------------------ cell pool
+// Slot map of the per-context cell pool.  Every slot is one cell vector of
+// nc doubles (owned rows first, then ghost cells); multi-component fields
+// occupy consecutive slots, so component c of a field is base + c*nc.
+enum Slot : int {
+  S_U = 0,        // u, 3 slots
+  S_P = 3,        // p
+  S_HV = 4,       // HbyA, 3
+  S_RAU = 7,      // rAU
+  S_GU = 8,       // grad u, 9
+  S_GP = 17,      // grad p, 3
+  S_AU = 20,      // A u, 3
+  S_B0 = 23,      // momentum rhs b0, 3
+  S_RHS = 26,     // momentum solve rhs, 3
+  S_DIAG = 29,    // momentum diagonal
+  S_DIVH = 30,    // div(phiHbyA)
+  S_RL = 31,      // pressure Laplacian rhs
+  S_RP = 32,      // pressure solve rhs
+  S_PBEFORE = 33, // p before the SIMPLE correction
+  S_SCR = 34,     // solver scratch
+  kScrSlots = 26, // BiCGStab x3: inv + 8 vectors per component + spare
+  kPoolSlots = S_SCR + kScrSlots,
+};
+
+// Team comm area at the head of the pool (shared with the peers).
+struct Comm {
+  unsigned long long seq[kMaxTeam];              // written by peers: last epoch seen
+  unsigned long long epoch;                      // local: team syncs completed
+  unsigned long long pad[7];
+  double mail[2][kMaxTeam][kMailM];              // [epoch parity][sender][payload]
+};
+constexpr size_t kCommBytes = 4096;
+static_assert(sizeof(Comm) <= kCommBytes, "comm area");
+
+// Device view of the team: who the peers are and where their pools are.
+struct TeamView {
+  int rank, size;             // size 1 = no decomposition
+  Comm* comm;                 // local comm area
+  Comm* peer_comm[kMaxTeam];  // every rank's comm area (own included)
+  double* peer_cells[kMaxTeam];  // every rank's slot 0 base
+  int peer_nc[kMaxTeam];      // every rank's slot stride
+  // halo sends: owned rows >= n_inner send their values; row i sends
+  // entries send_ptr[i-n_inner] .. send_ptr[i-n_inner+1] to
+  // (send_rank[e], ghost index send_dst[e])
+  int n_inner;
+  const int* send_ptr;
+  const int* send_rank;
+  const int* send_dst;
+};
+
+// Store value v of row i (pool slot `slot`) into the ghost copies held by
+// the ranks that need it.
+__device__ __forceinline__ void halo_send(const TeamView& T, int i, int slot, double v) {
+  const int t = i - T.n_inner;
+  const int e1 = T.send_ptr[t + 1];
+  for (int e = T.send_ptr[t]; e < e1; ++e) {
+    const int q = T.send_rank[e];
+    T.peer_cells[q][size_t(slot) * T.peer_nc[q] + T.send_dst[e]] = v;
+  }
+}
 
 // ------------------------------------------------------------ device views
 // Face numbering follows the reference: internal faces [0, ni), boundary
-// faces [ni, nf); boundary arrays are indexed j = f - ni.
+// faces [ni, nf); boundary arrays are indexed j = f - ni.  Row loops run
+// over the nr owned cells; vectors hold nc = nr + ghosts entries.
 struct MeshView {
-  int nc, nf, ni, nb;
+  int nc, nr, nf, ni, nb;
   const int* own;     // [nf]
   const int* nbr;     // [ni]
   const double* sx;   // area vector S, SoA [nf]
@@ -53,13 +124,13 @@ struct MeshView {
   const double* kx;   // S - a d      [nf]
   const double* ky;
   const double* kz;
-  const int* cf_ptr;  // per-cell face list [nc+1]
+  const int* cf_ptr;  // per-row face list [nr+1]
   const int* cf;      // f for owned faces, ~f for neighbour faces
 };
 
 struct PatternView {
-  int n, k, nnz_crs;
-  const int* I;          // slot-major [k*n], -1 padding
+  int n, k, nnz_crs;     // n = rows (slot stride of V and I)
+  const int* I;          // slot-major [k*n], -1 padding, columns < nc
   const int* diag_slot;  // [n]
   const int* slot_face;  // slot-major [k*n]: internal face of the entry, -1
   const int* crs_ptr;    // [n+1] (nullptr when nnz_crs == 0)
@@ -83,15 +154,10 @@ struct MatView {
 };
 
 // --------------------------------------------------------------- context
-template <typename T>
-struct DBuf {
-  T* p = nullptr;
-  size_t n = 0;
-};
-
 struct Ctx {
   int dev = 0;
   int num_sms = 148;
+  int sm_share = 1;                 // teams sharing one device (tests): grid / sm_share
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8];
   cudaEvent_t tev[2];
@@ -99,7 +165,7 @@ struct Ctx {
   int64_t bytes = 0;
   bool have_mesh = false, have_pattern = false;
   bool have_bc[2] = {false, false};
-  int nc = 0, nf = 0, ni = 0, nb = 0, k = 0, nnz_crs = 0;
+  int nc = 0, nr = 0, nf = 0, ni = 0, nb = 0, k = 0, nnz_crs = 0;
   int first_zero_dmag = -1;          // coincident-centroid internal face
   int first_zero_dbmag_value[2] = {-1, -1};
   std::vector<double> dbmag_host;    // boundary |d_b| (for BC checks)
@@ -117,26 +183,47 @@ struct Ctx {
   int* bc_patch[2] = {nullptr, nullptr};
   double* bc_fixed[2] = {nullptr, nullptr};
   double* bc_speed[2] = {nullptr, nullptr};
-  // coupled state (SoA)
+  // cell pool (comm area + kPoolSlots vectors of nc doubles)
+  char* pool = nullptr;
+  double* cells = nullptr;           // slot 0
+  // coupled state on the device (faces/boundary arrays outside the pool)
   double *u = nullptr, *p = nullptr, *flux = nullptr, *ub = nullptr, *pb = nullptr;
+  // team
+  TeamView team{};
+  int* send_ptr = nullptr;
+  int* send_rank = nullptr;
+  int* send_dst = nullptr;
+  // step work (allocated once, at upload time: never inside a step, where a
+  // peer rank may be spinning in a team sync)
+  bool work_ready = false;
+  double *Vm = nullptr, *crsm = nullptr, *Vp = nullptr, *crsp = nullptr, *phih = nullptr,
+         *rauf = nullptr, *coef = nullptr, *corr = nullptr, *lf = nullptr;
   // work
   std::vector<void*> allocs;
-  double* scratch = nullptr;  // general work pool
-  size_t scratch_n = 0;
-  unsigned* sync = nullptr;   // grid barrier words + error slots
+  double* scratch = nullptr;  // solver scratch (pool slots S_SCR..)
+  unsigned* sync = nullptr;   // grid barrier words + broadcast slots
   double* partials = nullptr;
   int* ipart = nullptr;
-  double* host_pinned = nullptr;  // small pinned staging buffer
 
+  double* slot(int s) const { return cells + size_t(s) * nc; }
+  int slot_of(const double* q) const {
+    if (!cells || q < cells) return -1;
+    const size_t off = size_t(q - cells);
+    if (off % size_t(nc)) return -1;
+    const size_t s = off / size_t(nc);
+    return s < size_t(kPoolSlots) ? int(s) : -1;
+  }
   MeshView mesh() const {
-    return MeshView{nc, nf, ni, nb, own, nbr, sx, sy, sz, smag, vol, w, a, kx, ky, kz, cf_ptr, cf};
+    return MeshView{nc, nr, nf, ni, nb, own, nbr, sx, sy, sz, smag, vol, w, a, kx, ky, kz,
+                    cf_ptr, cf};
   }
   PatternView pattern() const {
-    return PatternView{nc, k, nnz_crs, I, diag_slot, slot_face, crs_ptr, crs_col, crs_face};
+    return PatternView{nr, k, nnz_crs, I, diag_slot, slot_face, crs_ptr, crs_col, crs_face};
   }
   BcView bc(int field) const {
     return BcView{bc_kind[field], bc_patch[field], bc_fixed[field], bc_speed[field]};
   }
+  bool teamed() const { return team.size > 1; }
 };
 
 template <typename T>
@@ -153,6 +240,9 @@ int dalloc(Ctx* c, T** out, size_t n) {
   *out = static_cast<T*>(p);
   return FVB_OK;
 }
+
+// create the cell pool once nc is known (mesh or pattern upload)
+int ensure_pool(Ctx* c);
 
 // ------------------------------------------------------- kernel helpers
 inline int grid_for(int64_t n, int threads, int cap = 148 * 32) {
@@ -173,7 +263,6 @@ __device__ __forceinline__ double ell_row(const double* __restrict__ V,
   double ev = 0.0, od = 0.0;
 #pragma unroll
   for (int s = 0; s < (KT > 0 ? KT : K); s += 2) {
-    if (KT == 0 && s >= K) break;
     int col = __ldg(I + size_t(s) * n + i);
     double v = __ldg(V + size_t(s) * n + i);
     double pr = v * gather(col < 0 ? 0 : col);
@@ -181,7 +270,6 @@ __device__ __forceinline__ double ell_row(const double* __restrict__ V,
   }
 #pragma unroll
   for (int s = 1; s < (KT > 0 ? KT : K); s += 2) {
-    if (KT == 0 && s >= K) break;
     int col = __ldg(I + size_t(s) * n + i);
     double v = __ldg(V + size_t(s) * n + i);
     double pr = v * gather(col < 0 ? 0 : col);
@@ -234,74 +322,137 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
-// Grid-wide barrier for co-resident (cooperatively launched) grids.
-// sync[0] = arrival count, sync[1] = generation, sync[2] = abort flag.
-// A watchdog turns a would-be hang into FVB_E_TIMEOUT instead of a dead GPU.
-__device__ __forceinline__ bool grid_barrier(unsigned* sync, unsigned nblocks) {
-  __syncthreads();
-  __shared__ int s_abort;
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = sync + 1;
-    volatile unsigned* vabort = sync + 2;
-    unsigned gen = *vgen;
-    __threadfence();
-    unsigned arrived = atomicAdd(sync, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(sync, 0u);
-      __threadfence();
-      atomicAdd(sync + 1, 1u);
-    } else {
-      uint64_t t0 = global_ns();
-      while (*vgen == gen) {
-        if (*vabort) break;
-        __nanosleep(20);
-        if (global_ns() - t0 > 20000000000ull) {  // 20 s watchdog
-          atomicExch(sync + 2, 1u);
-          break;
-        }
-      }
-    }
-    __threadfence();
-    s_abort = *vabort;
-  }
-  __syncthreads();
-  return s_abort == 0;
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// After a barrier: every block sums the per-block partials of M scalars in
-// the same fixed order, so all blocks hold bit-identical results.
+constexpr uint64_t kWatchdogNs = 20000000000ull;  // 20 s: a hang becomes FVB_E_TIMEOUT
+
+enum ReduceOp { RED_SUM = 0, RED_MAX = 1, RED_MIN = 2 };
+
+// Exchange M doubles with every rank of the team and combine them in rank
+// order (identical on every rank).  Called by ONE thread.  Returns false
+// when the watchdog fired.  Epoch parity double-buffers the mailboxes: a
+// rank can run at most one sync ahead of the slowest reader.
 template <int M>
-__device__ __forceinline__ void grid_sum(const double* partials, int nblocks,
-                                         double (&out)[M], double* smem) {
+__device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
+  Comm* me = T.comm;
+  volatile unsigned long long* vep = &me->epoch;  // written by other blocks' SMs
+  const unsigned long long ep = *vep + 1;
+  *vep = ep;
+  const int par = int(ep & 1ull);
+  __threadfence_system();  // order this rank's halo stores before the message
+  for (int q = 0; q < T.size; ++q) {
+    Comm* pc = T.peer_comm[q];
+#pragma unroll
+    for (int m = 0; m < M; ++m) pc->mail[par][T.rank][m] = v[m];
+  }
+  __threadfence_system();
+  for (int q = 0; q < T.size; ++q) st_release_sys(&T.peer_comm[q]->seq[T.rank], ep);
+  const uint64_t t0 = global_ns();
+  for (int q = 0; q < T.size; ++q) {
+    while (ld_acquire_sys(&me->seq[q]) < ep) {
+      if (global_ns() - t0 > kWatchdogNs) return false;
+      __nanosleep(32);
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+    const volatile double* box = &me->mail[par][0][m];
+    double acc = box[0];
+    for (int q = 1; q < T.size; ++q) {
+      const double x = box[q * kMailM];
+      acc = op == RED_SUM ? acc + x : (op == RED_MAX ? fmax(acc, x) : fmin(acc, x));
+    }
+    v[m] = acc;
+  }
+  return true;
+}
+
+// Grid(+team)-wide deterministic sum of M doubles for co-resident
+// (cooperatively launched) grids.  v holds each thread's partial sums on
+// entry and the global sums on exit, bit-identical in every thread of every
+// block of every rank.  Block partials are summed by the last block to
+// arrive in a fixed order (lane-strided over blocks, then a shuffle tree),
+// the team combine goes through the peer mailboxes, and the result is
+// broadcast through the sync area.  sync words: [0] arrivals, [1]
+// generation, [2] abort flag, [4..) broadcast doubles.  The barrier also
+// orders every halo store issued before it.  Returns false on watchdog.
+template <int M>
+__device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
+                                            double* partials, double (&v)[M],
+                                            double* smem /*[32*M+M]*/) {
+  __shared__ int s_last, s_ok;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (warp == 0) {
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      double x = 0.0;
-      for (int b = lane; b < nblocks; b += 32) x += __ldcg(partials + size_t(m) * nblocks + b);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-      if (lane == 0) smem[m] = x;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int m = 0; m < M; ++m) out[m] = smem[m];
-  __syncthreads();
-}
-
-template <int M>
-__device__ __forceinline__ void publish_partials(double (&v)[M], double* partials,
-                                                 double* smem) {
   block_reduce<M>(v, smem);
+  volatile unsigned* vgen = sync + 1;
+  volatile unsigned* vabort = sync + 2;
+  double* bcast = reinterpret_cast<double*>(sync + 4);
+  unsigned gen = 0;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int m = 0; m < M; ++m) partials[size_t(m) * gridDim.x + blockIdx.x] = v[m];
+    gen = *vgen;
+    if (T.size > 1) __threadfence_system(); else __threadfence();
+    s_last = atomicAdd(sync, 1u) == gridDim.x - 1;
   }
+  __syncthreads();
+  if (s_last) {
+    if (warp == 0) {
+      __threadfence();
+      double r[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double x = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32)
+          x += __ldcg(partials + size_t(m) * gridDim.x + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        r[m] = x;
+      }
+      if (lane == 0) {
+        bool ok = true;
+        if (T.size > 1) ok = team_exchange<M>(T, r, RED_SUM);
+        if (!ok) *vabort = 1u;
+#pragma unroll
+        for (int m = 0; m < M; ++m) __stcg(bcast + m, r[m]);
+        atomicExch(sync, 0u);
+        __threadfence();
+        atomicAdd(sync + 1, 1u);
+      }
+    }
+  } else if (threadIdx.x == 0) {
+    const uint64_t t0 = global_ns();
+    while (*vgen == gen) {
+      if (*vabort) break;
+      __nanosleep(20);
+      if (global_ns() - t0 > kWatchdogNs + 2000000000ull) {
+        atomicExch(sync + 2, 1u);
+        break;
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();  // gpu-scope fence: also invalidates this SM's L1
+    s_ok = *vabort == 0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) smem[32 * M + m] = __ldcg(bcast + m);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
+  const bool ok = s_ok != 0;
+  __syncthreads();
+  return ok;
 }
 
 // ------------------------------------------------------------ launchers
-// (implemented in fvb_ops.cu / fvb_solvers.cu)
+// (implemented in fvb_ops.cu / fvb_solvers.cu / fvb_team.cu)
 int launch_inv_diag(Ctx* c, const double* V, double* inv, int* first_zero);
 int smvp(Ctx* c, MatView A, const double* x, double* y);
 
@@ -320,7 +471,7 @@ enum SolveErr {
   SE_OMEGA = 6,
   SE_TIMEOUT = 7,
 };
-// x must hold x0 on entry; returns solution in x.
+// x must hold x0 on entry (ghost entries current); returns solution in x.
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol,
              double abs_tol, int max_iters, SolveOut* out);
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
@@ -328,7 +479,13 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
                    SolveOut* out);
 std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row);
 
-// FV operators on device buffers (fvb_ops.cu)
+// team collectives (fvb_team.cu): halo exchange of consecutive pool slots
+// and a small allreduce; both are no-ops for a context without a team.
+int team_halo(Ctx* c, int first_slot, int nslots);
+int team_allreduce(Ctx* c, double* host_vals, int m, int op);
+
+// FV operators on device buffers (fvb_ops.cu); multi-component vectors use
+// component stride nc (the pool layout).
 int op_apply_bcs(Ctx* c, int field, int ncomp, const double* vals, double* bnd);
 int op_interp(Ctx* c, int field, int ncomp, const double* vals, const double* bnd,
               double* fv);

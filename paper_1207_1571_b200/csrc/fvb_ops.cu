@@ -90,7 +90,7 @@ template <int NC>
 __global__ void k_gradient(MeshView M, BcView B, const double* __restrict__ vals,
                            const double* __restrict__ bnd, double* __restrict__ grad) {
   // gauss_gradient (fvm.py:258-275): owner faces then neighbour faces, / V
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < M.nc; c += gridDim.x * blockDim.x) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < M.nr; c += gridDim.x * blockDim.x) {
     double g[NC][3];
 #pragma unroll
     for (int i = 0; i < NC; ++i) g[i][0] = g[i][1] = g[i][2] = 0.0;
@@ -120,7 +120,7 @@ __global__ void k_gradient(MeshView M, BcView B, const double* __restrict__ vals
 
 __global__ void k_divergence(MeshView M, const double* __restrict__ flux, double* __restrict__ div) {
   // face_divergence (fvm.py:250-255)
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < M.nc; c += gridDim.x * blockDim.x) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < M.nr; c += gridDim.x * blockDim.x) {
     double acc = 0.0;
     const int e1 = M.cf_ptr[c + 1];
     for (int e = M.cf_ptr[c]; e < e1; ++e) {
@@ -171,7 +171,8 @@ __global__ void k_laplacian_rows(MeshView M, PatternView P, BcView B, LapArgs L,
                                  double* __restrict__ rhs, const double* __restrict__ bnd,
                                  const double* __restrict__ grad) {
   // laplacian (fvm.py:335-408), one matrix row per thread
-  const int n = M.nc;
+  const int n = P.n;            // rows = slot stride of V
+  const size_t nv = M.nc;       // component stride of cell vectors
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const int e0 = M.cf_ptr[c], e1 = M.cf_ptr[c + 1];
     const int ds = P.diag_slot[c];
@@ -207,7 +208,7 @@ __global__ void k_laplacian_rows(MeshView M, PatternView P, BcView B, LapArgs L,
     // right-hand side
     double r[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) r[i] = rhs[size_t(i) * n + c];
+    for (int i = 0; i < NC; ++i) r[i] = rhs[size_t(i) * nv + c];
     if (NC == 3) {
       // vector branch: fancy-index "-=", the highest-index face wins (fvm.py:378-379)
       if (last_value >= 0) {
@@ -250,7 +251,7 @@ __global__ void k_laplacian_rows(MeshView M, PatternView P, BcView B, LapArgs L,
       }
     }
 #pragma unroll
-    for (int i = 0; i < NC; ++i) rhs[size_t(i) * n + c] = r[i];
+    for (int i = 0; i < NC; ++i) rhs[size_t(i) * nv + c] = r[i];
   }
 }
 
@@ -294,7 +295,8 @@ __global__ void k_convection_rows(MeshView M, PatternView P, BcView B, MatView A
                                   double* __restrict__ rhs, const double* __restrict__ flux,
                                   const double* __restrict__ bnd, int linear, double coeff) {
   // divergence_convection (fvm.py:432-482), one matrix row per thread
-  const int n = M.nc;
+  const int n = P.n;            // rows = slot stride of V
+  const size_t nv = M.nc;       // component stride of cell vectors
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const int e0 = M.cf_ptr[c], e1 = M.cf_ptr[c + 1];
     const int ds = P.diag_slot[c];
@@ -356,7 +358,7 @@ __global__ void k_convection_rows(MeshView M, PatternView P, BcView B, MatView A
         const int j = last_value - M.ni;
 #pragma unroll
         for (int i = 0; i < NC; ++i)
-          rhs[size_t(i) * n + c] = rhs[size_t(i) * n + c] - cb * bnd[size_t(i) * M.nb + j];
+          rhs[size_t(i) * nv + c] = rhs[size_t(i) * nv + c] - cb * bnd[size_t(i) * M.nb + j];
       }
     } else {
       double r = rhs[c];
@@ -372,15 +374,16 @@ __global__ void k_convection_rows(MeshView M, PatternView P, BcView B, MatView A
   }
 }
 
-__global__ void k_ddt(int n, PatternView P, MatView A, int ncomp, double* __restrict__ rhs,
+__global__ void k_ddt(int nv, PatternView P, MatView A, int ncomp, double* __restrict__ rhs,
                       const double* __restrict__ old, const double* __restrict__ vol, double dt,
                       double coeff) {
-  // ddt_euler (fvm.py:485-496)
+  // ddt_euler (fvm.py:485-496); rows P.n, cell vectors strided by nv
+  const int n = P.n;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
     const double vdt = (coeff * vol[c]) / dt;
     const int ds = P.diag_slot[c];
     A.V[size_t(ds) * n + c] += vdt;
-    for (int i = 0; i < ncomp; ++i) rhs[size_t(i) * n + c] += vdt * old[size_t(i) * n + c];
+    for (int i = 0; i < ncomp; ++i) rhs[size_t(i) * nv + c] += vdt * old[size_t(i) * nv + c];
   }
 }
 
@@ -449,17 +452,17 @@ int op_interp(Ctx* c, int field, int ncomp, const double* vals, const double* bn
 int op_gradient(Ctx* c, int field, int ncomp, const double* vals, const double* bnd,
                 double* grad) {
   if (ncomp == 1)
-    { k_gradient<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
+    { k_gradient<1><<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
                                                                          vals, bnd, grad); fvb::note_launch(); }
   else
-    { k_gradient<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
+    { k_gradient<3><<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field),
                                                                          vals, bnd, grad); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
 
 int op_divergence(Ctx* c, const double* flux, double* div) {
-  { k_divergence<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->mesh(), flux, div); fvb::note_launch(); }
+  { k_divergence<<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(c->mesh(), flux, div); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }
@@ -479,13 +482,13 @@ int op_laplacian(Ctx* c, int field, int ncomp, MatView A, double* rhs, double ga
   }
   LapArgs L{gamma, gamma_faces, coeff, nonorth && limiter > 0.0, limiter};
   if (ncomp == 1) {
-    { k_laplacian_rows<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+    { k_laplacian_rows<1><<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(
         c->mesh(), c->pattern(), c->bc(field), L, A, rhs, bnd, grad); fvb::note_launch(); }
     if (coef)
       { k_laplacian_faces<1><<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
           c->mesh(), c->bc(field), L, grad, coef, corr); fvb::note_launch(); }
   } else {
-    { k_laplacian_rows<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+    { k_laplacian_rows<3><<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(
         c->mesh(), c->pattern(), c->bc(field), L, A, rhs, bnd, grad); fvb::note_launch(); }
     if (coef)
       { k_laplacian_faces<3><<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
@@ -506,10 +509,10 @@ int op_lap_flux(Ctx* c, int field, int ncomp, const double* coef, const double* 
 int op_convection(Ctx* c, int field, int ncomp, MatView A, double* rhs, const double* flux,
                   const double* bnd, int scheme, double coeff) {
   if (ncomp == 1)
-    { k_convection_rows<1><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+    { k_convection_rows<1><<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(
         c->mesh(), c->pattern(), c->bc(field), A, rhs, flux, bnd, scheme, coeff); fvb::note_launch(); }
   else
-    { k_convection_rows<3><<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(
+    { k_convection_rows<3><<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(
         c->mesh(), c->pattern(), c->bc(field), A, rhs, flux, bnd, scheme, coeff); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
@@ -517,7 +520,7 @@ int op_convection(Ctx* c, int field, int ncomp, MatView A, double* rhs, const do
 
 int op_ddt(Ctx* c, int ncomp, MatView A, double* rhs, const double* old, double dt,
            double coeff) {
-  { k_ddt<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->nc, c->pattern(), A, ncomp, rhs,
+  { k_ddt<<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(c->nc, c->pattern(), A, ncomp, rhs,
                                                                old, c->vol, dt, coeff); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
@@ -533,7 +536,7 @@ int op_face_flux(Ctx* c, int ncomp_field, const double* vals, const double* bnd,
 }
 
 int launch_inv_diag(Ctx* c, const double* V, double* inv, int* first_zero) {
-  { k_inv_diag<<<grid_for(c->nc, kThreads), kThreads, 0, c->stream>>>(c->nc, c->diag_slot, V, inv,
+  { k_inv_diag<<<grid_for(c->nr, kThreads), kThreads, 0, c->stream>>>(c->nr, c->diag_slot, V, inv,
                                                                      first_zero); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
@@ -541,7 +544,7 @@ int launch_inv_diag(Ctx* c, const double* V, double* inv, int* first_zero) {
 
 int smvp(Ctx* c, MatView A, const double* x, double* y) {
   PatternView P = c->pattern();
-  const int g = grid_for(c->nc, kThreads);
+  const int g = grid_for(c->nr, kThreads);
   switch (c->k) {
     case 5: { k_smvp<5><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
     case 7: { k_smvp<7><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;

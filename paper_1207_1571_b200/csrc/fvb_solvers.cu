@@ -2,17 +2,20 @@
 // launched kernels (linsolve.py:102-282 restated for sm_100a).
 //
 // One launch runs a whole solve: rows are strided over the co-resident
-// grid, every global sync point is one grid barrier, and the dot products
-// are deterministic (fixed per-thread order -> warp-shuffle tree -> fixed
-// block order).  Every block re-reduces the per-block partials in the same
-// order, so all blocks hold identical scalars and take identical branches:
-// the reference's stopping rules (check on entry, break right after the
-// residual test, breakdown checks) run on the device with no host round
-// trip per iteration.
+// grid, every global sync point is one team_reduce (grid barrier + peer
+// mailbox exchange when the mesh is decomposed), and the dot products are
+// deterministic (fixed per-thread order -> warp-shuffle tree -> fixed block
+// order -> fixed rank order), so every block of every rank holds identical
+// scalars and takes identical branches: the reference's stopping rules
+// (check on entry, break right after the residual test, breakdown checks)
+// run on the device with no host round trip per iteration.
 //
 // CG is fused into two passes per iteration: pass A
 // rebuilds p = z + beta p on the fly for every gathered column while it
-// forms q = A p and p.q; pass B updates x and r and forms ||r||^2 and r.z.
+// forms q = A p and p.q; pass B updates x and r, stores z = r / D and forms
+// ||r||^2 and r.z.  Rows on a processor boundary store their fresh p (pass
+// A) and z (pass B) straight into the neighbour ranks' ghost slots; the
+// reduction that closes the pass orders those stores.
 #include <cmath>
 
 #include "fvb_internal.cuh"
@@ -27,15 +30,18 @@ constexpr double kTiny = 1e-300;      // linsolve.py:21
 
 struct CgParams {
   PatternView P;
+  TeamView T;
   const double* V;
   const double* crs;
   const double* inv;
   const double* b;
   double* x;
   double* r;
+  double* z;
   double* pa;
   double* pb;
   double* q;
+  int slot_z, slot_pa, slot_pb;  // pool slots (halo targets)
   double tol, abs_tol;
   int max_iters;
   unsigned* sync;
@@ -44,37 +50,38 @@ struct CgParams {
 };
 
 template <int KT>
-__global__ void __launch_bounds__(kSolverThreads) k_cg(CgParams A) {
-  __shared__ double red[32 * 4];
-  __shared__ double sc[8];
+__global__ void __launch_bounds__(kSolverThreads, 2) k_cg(CgParams A) {
+  __shared__ double red[32 * 3 + 3];
   const PatternView& P = A.P;
+  const TeamView& T = A.T;
   const int n = P.n;
-  const int T = gridDim.x * blockDim.x;
+  const int G = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
 
-  // setup: r = b - A x0, ||b||, ||r||, r.z  (linsolve.py:106-127)
+  // setup: r = b - A x0, z = r / D, ||b||, ||r||, r.z  (linsolve.py:106-127)
+  double s3[3] = {0.0, 0.0, 0.0};
   {
-    double acc[3] = {0.0, 0.0, 0.0};
     const double* x = A.x;
-    for (int i = tid; i < n; i += T) {
+    for (int i = tid; i < n; i += G) {
       auto g = [&](int col) { return x[col]; };
-      double ax = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
+      const double ax = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
       const double bi = A.b[i];
       const double ri = bi - ax;
+      const double zi = ri * inv[i];
       A.r[i] = ri;
-      acc[0] += bi * bi;
-      acc[1] += ri * ri;
-      acc[2] += ri * (ri * inv[i]);
+      A.z[i] = zi;
+      if (team && i >= T.n_inner) halo_send(T, i, A.slot_z, zi);
+      s3[0] += bi * bi;
+      s3[1] += ri * ri;
+      s3[2] += ri * zi;
     }
-    publish_partials<3>(acc, A.partials, red);
   }
-  if (!grid_barrier(A.sync, gridDim.x)) {
+  if (!team_reduce<3>(T, A.sync, A.partials, s3, red)) {
     if (tid == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
-  double s3[3];
-  grid_sum<3>(A.partials, gridDim.x, s3, sc);
   const double bnorm = fmax(sqrt(s3[0]), kResFloor);
   double res = sqrt(s3[1]) / bnorm;
   const double res0 = res;
@@ -85,54 +92,49 @@ __global__ void __launch_bounds__(kSolverThreads) k_cg(CgParams A) {
   double beta = 0.0;
   double* pold = A.pa;
   double* pnew = A.pb;
+  int slot_new = A.slot_pb;
   bool first = true;
   while (!conv && it < A.max_iters) {
     ++it;
     // pass A: p <- z + beta p (gathered columns), q = A p, p.q
+    double pq[1] = {0.0};
     {
-      double acc[1] = {0.0};
-      const double* r = A.r;
-      const double* po = pold;
-      for (int i = tid; i < n; i += T) {
-        auto g = [&](int col) {
-          const double z = r[col] * inv[col];
-          return first ? z : po[col] * beta + z;
-        };
+      const double* __restrict__ z = A.z;
+      const double* __restrict__ po = pold;
+      for (int i = tid; i < n; i += G) {
+        auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
         const double qi = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
         const double pi = g(i);
         pnew[i] = pi;
         A.q[i] = qi;
-        acc[0] += pi * qi;
+        if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
+        pq[0] += pi * qi;
       }
-      publish_partials<1>(acc, A.partials, red);
     }
-    if (!grid_barrier(A.sync, gridDim.x)) { err = SE_TIMEOUT; break; }
-    double pq[1];
-    grid_sum<1>(A.partials, gridDim.x, pq, sc);
+    if (!team_reduce<1>(T, A.sync, A.partials, pq, red)) { err = SE_TIMEOUT; break; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
-    // pass B: x += alpha p, r -= alpha q, ||r||^2, r.z
-    {
-      double acc[2] = {0.0, 0.0};
-      for (int i = tid; i < n; i += T) {
-        const double pi = pnew[i];
-        A.x[i] = A.x[i] + alpha * pi;
-        const double ri = A.r[i] - alpha * A.q[i];
-        A.r[i] = ri;
-        acc[0] += ri * ri;
-        acc[1] += ri * (ri * inv[i]);
-      }
-      publish_partials<2>(acc, A.partials, red);
+    // pass B: x += alpha p, r -= alpha q, z = r / D, ||r||^2, r.z
+    double s2[2] = {0.0, 0.0};
+    for (int i = tid; i < n; i += G) {
+      const double pi = pnew[i];
+      A.x[i] = A.x[i] + alpha * pi;
+      const double ri = A.r[i] - alpha * A.q[i];
+      const double zi = ri * inv[i];
+      A.r[i] = ri;
+      A.z[i] = zi;
+      if (team && i >= T.n_inner) halo_send(T, i, A.slot_z, zi);
+      s2[0] += ri * ri;
+      s2[1] += ri * zi;
     }
-    if (!grid_barrier(A.sync, gridDim.x)) { err = SE_TIMEOUT; break; }
-    double s2[2];
-    grid_sum<2>(A.partials, gridDim.x, s2, sc);
+    if (!team_reduce<2>(T, A.sync, A.partials, s2, red)) { err = SE_TIMEOUT; break; }
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
     if (res <= A.tol || res * bnorm <= A.abs_tol) { conv = true; break; }
     beta = s2[1] / rz;
     rz = s2[1];
     double* t = pold; pold = pnew; pnew = t;
+    slot_new = (slot_new == A.slot_pb) ? A.slot_pa : A.slot_pb;
     first = false;
   }
   if (tid == 0) {
@@ -149,6 +151,7 @@ __global__ void __launch_bounds__(kSolverThreads) k_cg(CgParams A) {
 template <int NC>
 struct BiParams {
   PatternView P;
+  TeamView T;
   const double* V;
   const double* crs;
   const double* inv;
@@ -162,6 +165,7 @@ struct BiParams {
   double* s[NC];
   double* sh[NC];
   double* t[NC];
+  int slot_ph[NC], slot_sh[NC];  // pool slots (halo targets)
   double tol, abs_tol;
   int max_iters;
   unsigned* sync;
@@ -180,7 +184,6 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
   for (int c = 0; c < NC; ++c) ev[c] = od[c] = 0.0;
 #pragma unroll
   for (int s = 0; s < (KT > 0 ? KT : K); s += 2) {
-    if (KT == 0 && s >= K) break;
     int col = __ldg(P.I + size_t(s) * n + i);
     col = col < 0 ? 0 : col;
     const double v = __ldg(V + size_t(s) * n + i);
@@ -193,7 +196,6 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
   }
 #pragma unroll
   for (int s = 1; s < (KT > 0 ? KT : K); s += 2) {
-    if (KT == 0 && s >= K) break;
     int col = __ldg(P.I + size_t(s) * n + i);
     col = col < 0 ? 0 : col;
     const double v = __ldg(V + size_t(s) * n + i);
@@ -223,26 +225,27 @@ struct CompState {
 };
 
 template <int KT, int NC>
-__global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
-  __shared__ double red[32 * 2 * NC];
-  __shared__ double sc[2 * NC];
+__global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) {
+  __shared__ double red[32 * 2 * NC + 2 * NC];
   __shared__ CompState S[NC];
   const PatternView& P = A.P;
+  const TeamView& T = A.T;
   const int n = P.n;
-  const int T = gridDim.x * blockDim.x;
+  const int G = gridDim.x * blockDim.x;
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
   bool act[NC];
   bool timeout = false;
 
   // setup (linsolve.py:180-196)
+  double sums[2 * NC];
   {
-    double acc[2 * NC];
 #pragma unroll
-    for (int m = 0; m < 2 * NC; ++m) acc[m] = 0.0;
+    for (int m = 0; m < 2 * NC; ++m) sums[m] = 0.0;
 #pragma unroll
     for (int c = 0; c < NC; ++c) act[c] = true;
-    for (int i = tid; i < n; i += T) {
+    for (int i = tid; i < n; i += G) {
       double ax[NC];
       auto g = [&](int c, int col) { return A.x[c][col]; };
       ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, ax);
@@ -252,19 +255,16 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
         const double ri = bi - ax[c];
         A.r[c][i] = ri;
         A.rh[c][i] = ri;
-        acc[2 * c] += bi * bi;
-        acc[2 * c + 1] += ri * ri;
+        sums[2 * c] += bi * bi;
+        sums[2 * c + 1] += ri * ri;
       }
     }
-    publish_partials<2 * NC>(acc, A.partials, red);
   }
-  if (!grid_barrier(A.sync, gridDim.x)) {
+  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red)) {
     if (tid == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
   }
-  double sums[2 * NC];
-  grid_sum<2 * NC>(A.partials, gridDim.x, sums, sc);
   if (threadIdx.x == 0) {
     for (int c = 0; c < NC; ++c) {
       CompState& s = S[c];
@@ -311,8 +311,9 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
     }
     if (!any) break;
     // pass P: p = r | p = (p - omega v) beta + r ; p_hat = p / D ; restart r_hat
-    for (int i = tid; i < n; i += T) {
+    for (int i = tid; i < n; i += G) {
       const double iv = inv[i];
+      const bool snd = team && i >= T.n_inner;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         if (!act[c]) continue;
@@ -326,17 +327,22 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
           pi = pi + ri;
         }
         A.p[c][i] = pi;
-        A.ph[c][i] = pi * iv;
+        const double phi = pi * iv;
+        A.ph[c][i] = phi;
+        if (snd) halo_send(T, i, A.slot_ph[c], phi);
         if (S[c].restart) A.rh[c][i] = ri;
       }
     }
-    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
+    {
+      double z1[1] = {0.0};
+      if (!team_reduce<1>(T, A.sync, A.partials, z1, red)) { timeout = true; break; }
+    }
     // pass V: v = A p_hat, r_hat.v
     {
-      double acc[NC];
+      double rv[NC];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-      for (int i = tid; i < n; i += T) {
+      for (int c = 0; c < NC; ++c) rv[c] = 0.0;
+      for (int i = tid; i < n; i += G) {
         double y[NC];
         auto g = [&](int c, int col) { return A.ph[c][col]; };
         ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
@@ -344,15 +350,10 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
           A.v[c][i] = y[c];
-          acc[c] += A.rh[c][i] * y[c];
+          rv[c] += A.rh[c][i] * y[c];
         }
       }
-      publish_partials<NC>(acc, A.partials, red);
-    }
-    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
-    {
-      double rv[NC];
-      grid_sum<NC>(A.partials, gridDim.x, rv, sc);
+      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red)) { timeout = true; break; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
@@ -365,26 +366,24 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
     }
     // pass S: s = r - alpha v, s_hat = s / D, ||s||^2
     {
-      double acc[NC];
+      double ss[NC];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-      for (int i = tid; i < n; i += T) {
+      for (int c = 0; c < NC; ++c) ss[c] = 0.0;
+      for (int i = tid; i < n; i += G) {
         const double iv = inv[i];
+        const bool snd = team && i >= T.n_inner;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
           const double si = A.r[c][i] - S[c].alpha * A.v[c][i];
           A.s[c][i] = si;
-          A.sh[c][i] = si * iv;
-          acc[c] += si * si;
+          const double shi = si * iv;
+          A.sh[c][i] = shi;
+          if (snd) halo_send(T, i, A.slot_sh[c], shi);
+          ss[c] += si * si;
         }
       }
-      publish_partials<NC>(acc, A.partials, red);
-    }
-    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
-    {
-      double ss[NC];
-      grid_sum<NC>(A.partials, gridDim.x, ss, sc);
+      if (!team_reduce<NC>(T, A.sync, A.partials, ss, red)) { timeout = true; break; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
@@ -401,10 +400,10 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
 #pragma unroll
     for (int c = 0; c < NC; ++c) tact[c] = act[c] && !S[c].sconv;
     {
-      double acc[2 * NC];
+      double tts[2 * NC];
 #pragma unroll
-      for (int m = 0; m < 2 * NC; ++m) acc[m] = 0.0;
-      for (int i = tid; i < n; i += T) {
+      for (int m = 0; m < 2 * NC; ++m) tts[m] = 0.0;
+      for (int i = tid; i < n; i += G) {
 #pragma unroll
         for (int c = 0; c < NC; ++c)
           if (act[c] && S[c].sconv) A.x[c][i] = A.x[c][i] + S[c].alpha * A.ph[c][i];
@@ -415,16 +414,11 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
         for (int c = 0; c < NC; ++c) {
           if (!tact[c]) continue;
           A.t[c][i] = y[c];
-          acc[2 * c] += y[c] * y[c];
-          acc[2 * c + 1] += y[c] * A.s[c][i];
+          tts[2 * c] += y[c] * y[c];
+          tts[2 * c + 1] += y[c] * A.s[c][i];
         }
       }
-      publish_partials<2 * NC>(acc, A.partials, red);
-    }
-    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
-    {
-      double tts[2 * NC];
-      grid_sum<2 * NC>(A.partials, gridDim.x, tts, sc);
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red)) { timeout = true; break; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
@@ -440,10 +434,10 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
     }
     // pass X: x += alpha p_hat; x += omega s_hat; r = s - omega t; ||r||^2, r_hat.r
     {
-      double acc[2 * NC];
+      double rr[2 * NC];
 #pragma unroll
-      for (int m = 0; m < 2 * NC; ++m) acc[m] = 0.0;
-      for (int i = tid; i < n; i += T) {
+      for (int m = 0; m < 2 * NC; ++m) rr[m] = 0.0;
+      for (int i = tid; i < n; i += G) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           if (!tact[c]) continue;
@@ -452,16 +446,11 @@ __global__ void __launch_bounds__(kSolverThreads) k_bicgstab(BiParams<NC> A) {
           A.x[c][i] = xi;
           const double ri = A.s[c][i] - S[c].omega * A.t[c][i];
           A.r[c][i] = ri;
-          acc[2 * c] += ri * ri;
-          acc[2 * c + 1] += A.rh[c][i] * ri;
+          rr[2 * c] += ri * ri;
+          rr[2 * c + 1] += A.rh[c][i] * ri;
         }
       }
-      publish_partials<2 * NC>(acc, A.partials, red);
-    }
-    if (!grid_barrier(A.sync, gridDim.x)) { timeout = true; break; }
-    {
-      double rr[2 * NC];
-      grid_sum<2 * NC>(A.partials, gridDim.x, rr, sc);
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red)) { timeout = true; break; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!tact[c]) continue;
@@ -495,7 +484,8 @@ int coop_blocks(Ctx* c, K kernel, int* blocks) {
     return FVB_E_CUDA;
   }
   if (per_sm > 2) per_sm = 2;
-  *blocks = per_sm * c->num_sms;
+  const int b = per_sm * c->num_sms / (c->sm_share > 0 ? c->sm_share : 1);
+  *blocks = b < 1 ? 1 : b;
   return FVB_OK;
 }
 
@@ -503,14 +493,25 @@ template <typename K, typename Args>
 int coop_launch(Ctx* c, K kernel, Args& args) {
   int blocks = 0;
   FVB_TRY(coop_blocks(c, kernel, &blocks));
-  FVB_CUDA(cudaMemsetAsync(c->sync, 0, 4 * sizeof(unsigned), c->stream));
+  // words 0-2: arrivals, generation, abort; word 3 (team error) is sticky
+  FVB_CUDA(cudaMemsetAsync(c->sync, 0, 3 * sizeof(unsigned), c->stream));
   void* params[] = {&args};
   fvb::note_launch();
-  FVB_CUDA(cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads),
-                                       params, 0, c->stream));
+  if (c->sm_share > 1) {
+    // several ranks share this device: each grid is sized to 1/share of the
+    // resident capacity, so the ranks' grids are co-resident together; a
+    // plain launch avoids relying on concurrent cooperative launches
+    FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads), params, 0,
+                              c->stream));
+  } else {
+    FVB_CUDA(cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads),
+                                         params, 0, c->stream));
+  }
   return FVB_OK;
 }
 
+// inverse diagonal of the owned rows; a zero diagonal anywhere in the team
+// is reported on every rank (so no rank enters the solve alone)
 int check_zero_diag(Ctx* c, MatView A, double* inv, int* zero_row) {
   int* dz = c->ipart;
   const int big = 0x7fffffff;
@@ -518,6 +519,11 @@ int check_zero_diag(Ctx* c, MatView A, double* inv, int* zero_row) {
   FVB_TRY(launch_inv_diag(c, A.V, inv, dz));
   FVB_CUDA(cudaMemcpyAsync(zero_row, dz, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
+  if (c->teamed()) {
+    double v = double(*zero_row);
+    FVB_TRY(team_allreduce(c, &v, 1, RED_MIN));
+    *zero_row = int(v);
+  }
   return FVB_OK;
 }
 
@@ -554,15 +560,16 @@ std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row
   return buf;
 }
 
-// Work buffers live in the context scratch pool: layout per call.
+// Work vectors are pool slots S_SCR.. (so the ghost entries can be written
+// by the neighbour ranks).
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double abs_tol,
              int max_iters, SolveOut* out) {
-  const size_t n = c->nc;
-  double* inv = c->scratch;
-  double* r = inv + n;
-  double* pa = r + n;
-  double* pb = pa + n;
-  double* q = pb + n;
+  double* inv = c->slot(S_SCR + 0);
+  double* r = c->slot(S_SCR + 1);
+  double* z = c->slot(S_SCR + 2);
+  double* pa = c->slot(S_SCR + 3);
+  double* pb = c->slot(S_SCR + 4);
+  double* q = c->slot(S_SCR + 5);
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
   FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
@@ -572,7 +579,8 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
     out->error_iteration = zero_row;
     return FVB_OK;
   }
-  CgParams prm{c->pattern(), A.V, A.crs, inv, b, x, r, pa, pb, q, tol, abs_tol, max_iters,
+  CgParams prm{c->pattern(), c->team, A.V, A.crs, inv, b, x, r, z, pa, pb, q,
+               S_SCR + 2, S_SCR + 3, S_SCR + 4, tol, abs_tol, max_iters,
                c->sync, c->partials, result};
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
   switch (c->k) {
@@ -582,8 +590,11 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   }
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[6];
+  unsigned team_err = 0;
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  FVB_CUDA(cudaMemcpyAsync(&team_err, c->sync + 3, sizeof team_err, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
+  if (team_err) h[4] = SE_TIMEOUT;
   out->iterations = int(h[0]);
   out->converged = int(h[1]);
   out->res0 = h[2];
@@ -599,24 +610,26 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
 template <int NC>
 static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const* x, double tol,
                        double abs_tol, int max_iters, double* inv, double* result) {
-  const size_t n = c->nc;
   BiParams<NC> prm;
   prm.P = c->pattern();
+  prm.T = c->team;
   prm.V = A.V;
   prm.crs = A.crs;
   prm.inv = inv;
-  double* w = inv + n;
+  int s = S_SCR + 1;
   for (int k = 0; k < NC; ++k) {
     prm.b[k] = b[k];
     prm.x[k] = x[k];
-    prm.r[k] = w; w += n;
-    prm.rh[k] = w; w += n;
-    prm.p[k] = w; w += n;
-    prm.ph[k] = w; w += n;
-    prm.v[k] = w; w += n;
-    prm.s[k] = w; w += n;
-    prm.sh[k] = w; w += n;
-    prm.t[k] = w; w += n;
+    prm.r[k] = c->slot(s++);
+    prm.rh[k] = c->slot(s++);
+    prm.p[k] = c->slot(s++);
+    prm.slot_ph[k] = s;
+    prm.ph[k] = c->slot(s++);
+    prm.v[k] = c->slot(s++);
+    prm.s[k] = c->slot(s++);
+    prm.slot_sh[k] = s;
+    prm.sh[k] = c->slot(s++);
+    prm.t[k] = c->slot(s++);
   }
   prm.tol = tol;
   prm.abs_tol = abs_tol;
@@ -633,7 +646,7 @@ static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const*
 
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double* const* x,
                    double tol, double abs_tol, int max_iters, SolveOut* out) {
-  double* inv = c->scratch;
+  double* inv = c->slot(S_SCR + 0);
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
   FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
@@ -654,9 +667,13 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
     FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[18];
+  unsigned team_err = 0;
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof(double) * 6 * ncomp, cudaMemcpyDeviceToHost,
                            c->stream));
+  FVB_CUDA(cudaMemcpyAsync(&team_err, c->sync + 3, sizeof team_err, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
+  if (team_err)
+    for (int k = 0; k < ncomp; ++k) h[6 * k + 4] = SE_TIMEOUT;
   for (int k = 0; k < ncomp; ++k) {
     out[k].iterations = int(h[6 * k]);
     out[k].converged = int(h[6 * k + 1]);

@@ -96,8 +96,11 @@ class DeviceContext:
                                         P(fixed), n_patches))
 
 
-def bc_table(field, geom, t=0.0):
+def bc_table(field, geom, t=0.0, with_speeds=True):
     """Per-boundary-face kind/patch/fixed tables + per-patch speeds at t.
+
+    with_speeds=False skips the speeds (a subdomain's tables: the mass-flow
+    area is the whole patch's and comes from the global geometry).
 
     Encodes the reference's condition classes (fvm.py:37-105) for libfvb;
     the per-patch normal speed of timed / mass-flow inlets is evaluated on
@@ -126,6 +129,8 @@ def bc_table(field, geom, t=0.0):
             speeds[pi] = bc.u0 * np.sin(fvm.TWO_PI * bc.freq * t)
         elif isinstance(bc, fvm.FixedMassFlow):
             kinds[sl] = _lib.BC_MASS_FLOW
+            if not with_speeds:
+                continue
             faces = slice(p.start, p.start + p.count)
             area = float(geom.face_area_mag[faces].sum())
             if area <= 0.0:

@@ -1,0 +1,94 @@
+"""Domain-decomposed runs on the device.
+
+P ranks share one B200 here (one libfvb context and host thread per rank,
+each persistent solver grid on 1/P of the SMs); the kernels, halo stores
+and peer-mailbox reductions are the ones a multi-GPU run uses.  A team of
+one must be bitwise the single-domain run; a team of P must match it
+under the parity rules (fields to the CPU-vs-CPU noise floor, CG
+iterations +-1, BiCGStab +-2) and match the reference's golden steps.
+"""
+
+import numpy as np
+import pytest
+
+from golden_io import golden_case, rel
+from paper_1207_1571_b200 import cases
+from paper_1207_1571_b200.coupling import (
+    CouplingConfig, continuity_error, init_state, piso_time_step, simple_outer_iteration)
+from paper_1207_1571_b200.team import DecomposedRun
+
+pytestmark = pytest.mark.gpu
+
+
+def _single(case, cfg, steps):
+    st = init_state(case, cfg)
+    for _ in range(steps):
+        if cfg.algorithm == "piso":
+            piso_time_step(st, cfg)
+        else:
+            simple_outer_iteration(st, cfg)
+    return st
+
+
+def _team(case, cfg, steps, nparts):
+    run = DecomposedRun(case, cfg, nparts)
+    for _ in range(steps):
+        if cfg.algorithm == "piso":
+            run.piso_time_step(cfg)
+        else:
+            run.simple_outer_iteration(cfg)
+    return run
+
+
+def test_team_of_one_is_bitwise_single_domain():
+    case = cases.gen_cavity(8)
+    case.config.algorithm, case.config.dt = "piso", 0.1 / 8
+    cfg = CouplingConfig.from_case_config(case.config)
+    st = _single(case, cfg, 2)
+    run = _team(case, cfg, 2, 1)
+    u, p, flux = run.gather()
+    assert np.array_equal(u, st.u.values)
+    assert np.array_equal(p, st.p.values)
+    assert np.array_equal(flux, st.flux)
+    assert run.residual_log == st.residual_log
+    run.close()
+
+
+@pytest.mark.parametrize("name,nparts", [("cav6", 2), ("cav6", 3), ("pcav5", 2), ("pcav5", 4),
+                                         ("bfs2", 2), ("chan", 2), ("duct", 3), ("cav20", 2)])
+def test_team_matches_single_domain_and_reference(name, nparts):
+    case, g = golden_case(name)
+    cfg = CouplingConfig.from_case_config(case.config)
+    steps = int(g["steps"])
+    st = _single(case, cfg, steps)
+    run = _team(case, cfg, steps, nparts)
+    u, p, flux = run.gather()
+    for a, b in ((u, st.u.values), (p, st.p.values), (flux, st.flux)):
+        assert rel(a, b) < 1e-9
+    s = steps - 1
+    assert rel(u, g[f"s{s}_u"]) < 1e-8
+    assert rel(p, g[f"s{s}_p"]) < 1e-8
+    assert rel(flux, g[f"s{s}_flux"]) < 1e-8
+    two_d = case.mesh.n_cells in (48, 260, 400)
+    assert len(run.residual_log) == len(st.residual_log)
+    for a, b in zip(run.residual_log, st.residual_log):
+        assert a[:3] == b[:3]
+        if two_d and a[1] == "uz":
+            continue
+        assert abs(a[3] - b[3]) <= (1 if a[0] == "cg" else 2), (a, b)
+    assert run.continuity_error() <= max(1e-8 * np.abs(flux).max(), 1e-16)
+    run.close()
+
+
+def test_team_cavity24_four_ranks():
+    case = cases.gen_cavity(24)
+    case.config.algorithm, case.config.dt = "piso", 0.1 / 24
+    cfg = CouplingConfig.from_case_config(case.config)
+    st = _single(case, cfg, 2)
+    run = _team(case, cfg, 2, 4)
+    u, p, flux = run.gather()
+    assert rel(u, st.u.values) < 1e-9 and rel(p, st.p.values) < 1e-9 and rel(flux, st.flux) < 1e-9
+    for a, b in zip(run.residual_log, st.residual_log):
+        assert abs(a[3] - b[3]) <= (1 if a[0] == "cg" else 2), (a, b)
+    assert continuity_error(st) <= 1e-8 * np.abs(st.flux).max()
+    run.close()
