@@ -348,7 +348,8 @@ def run_ours(args):
     if D.world > 1:
         from paper_1207_1571_b200.team import RankRun
 
-        run = RankRun(case, cfg, D.rank, D.world, D.local, D.allgather)
+        dev = int(os.environ.get("FVB_DEVICE", D.local))  # override only for 1-GPU tests
+        run = RankRun(case, cfg, D.rank, D.world, dev, D.allgather)
         h = run.ctx.h
         step = lambda: run.piso_time_step(cfg)  # noqa: E731
         last_solves = lambda: run.last_solves  # noqa: E731

@@ -17,6 +17,7 @@
 // A) and z (pass B) straight into the neighbour ranks' ghost slots; the
 // reduction that closes the pass orders those stores.
 #include <cmath>
+#include <cstdlib>
 
 #include "fvb_internal.cuh"
 
@@ -49,14 +50,102 @@ struct CgParams {
   double* result;  // [iters, converged, res0, res, err_kind, err_iter]
 };
 
-template <int KT>
-__global__ void __launch_bounds__(kSolverThreads, 2) k_cg(CgParams A) {
-  __shared__ double red[32 * 3 + 3];
+// Pass A with the ELL loads software-pipelined: the I/V slots of the
+// thread's next row are in flight while the current row gathers p and
+// sums (fixed K only; same arithmetic and order as ell_row).
+template <bool STREAM, typename T>
+__device__ __forceinline__ T ld_mat(const T* p) {
+  // matrix slots are read once per pass: evict-first keeps the gathered
+  // vectors resident in L1/L2
+  if (STREAM) return __ldcs(p);
+  return __ldg(p);
+}
+
+template <int KT, bool STREAM>
+__device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double* __restrict__ z,
+                                                 const double* __restrict__ po,
+                                                 double* __restrict__ pnew, double beta,
+                                                 bool first, int slot_new, int i, int end,
+                                                 int step) {
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int n = P.n;
-  const int G = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int* __restrict__ I = P.I;
+  const double* __restrict__ V = A.V;
+  const bool team = T.size > 1;
+  double acc = 0.0;
+  int ci[KT];
+  double vi[KT];
+  if (i < end) {
+#pragma unroll
+    for (int s = 0; s < KT; ++s) {
+      ci[s] = ld_mat<STREAM>(I + size_t(s) * n + i);
+      vi[s] = ld_mat<STREAM>(V + size_t(s) * n + i);
+    }
+  }
+  auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
+  while (i < end) {
+    const int nx = i + step;
+    int cn[KT];
+    double vn[KT];
+    if (nx < end) {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) {
+        cn[s] = ld_mat<STREAM>(I + size_t(s) * n + nx);
+        vn[s] = ld_mat<STREAM>(V + size_t(s) * n + nx);
+      }
+    }
+    double pr[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * g(ci[s] < 0 ? 0 : ci[s]);
+    double ev = pr[0];
+#pragma unroll
+    for (int s = 2; s < KT; s += 2) ev = ev + pr[s];
+    double y = ev;
+    if (KT > 1) {
+      double od = pr[1];
+#pragma unroll
+      for (int s = 3; s < KT; s += 2) od = od + pr[s];
+      y = ev + od;
+    }
+    const double qi = crs_tail(P, A.crs, i, y, g);
+    const double pi = g(i);
+    pnew[i] = pi;
+    A.q[i] = qi;
+    if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
+    acc += pi * qi;
+#pragma unroll
+    for (int s = 0; s < KT; ++s) {
+      ci[s] = cn[s];
+      vi[s] = vn[s];
+    }
+    i = nx;
+  }
+  return acc;
+}
+
+// Row ownership: CONTIG = 0 grid-strides rows over all threads; CONTIG = 1
+// gives every block one contiguous chunk swept in blockDim steps, so the
+// +-1 and +-n neighbours a row gathers were loaded by the same SM moments
+// earlier (L1 hits) and only the +-n^2 ones come from L2.
+template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0>
+__global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
+  __shared__ double red[32 * 3 + 3];
+  const PatternView& P = A.P;
+  const TeamView& T = A.T;
+  const int nrows = P.n;
+  int row0, n, G;
+  if (CONTIG) {
+    const int chunk = ((nrows + gridDim.x - 1) / gridDim.x + 31) & ~31;
+    row0 = blockIdx.x * chunk + threadIdx.x;
+    n = min(nrows, (blockIdx.x + 1) * chunk);
+    G = blockDim.x;
+  } else {
+    row0 = blockIdx.x * blockDim.x + threadIdx.x;
+    n = nrows;
+    G = gridDim.x * blockDim.x;
+  }
+  const int tid = row0;
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
 
@@ -66,7 +155,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_cg(CgParams A) {
     const double* x = A.x;
     for (int i = tid; i < n; i += G) {
       auto g = [&](int col) { return x[col]; };
-      const double ax = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
+      const double ax = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, nrows, P.k, i, g), g);
       const double bi = A.b[i];
       const double ri = bi - ax;
       const double zi = ri * inv[i];
@@ -101,14 +190,19 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_cg(CgParams A) {
     {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
-      for (int i = tid; i < n; i += G) {
-        auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
-        const double qi = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, n, P.k, i, g), g);
-        const double pi = g(i);
-        pnew[i] = pi;
-        A.q[i] = qi;
-        if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
-        pq[0] += pi * qi;
+      if (PIPE && KT > 0) {
+        pq[0] = cg_pass_a_pipe<(KT > 0 ? KT : 1), (PIPE > 1)>(A, z, po, pnew, beta, first,
+                                                                slot_new, tid, n, G);
+      } else {
+        for (int i = tid; i < n; i += G) {
+          auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
+          const double qi = crs_tail(P, A.crs, i, ell_row<KT>(A.V, P.I, nrows, P.k, i, g), g);
+          const double pi = g(i);
+          pnew[i] = pi;
+          A.q[i] = qi;
+          if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
+          pq[0] += pi * qi;
+        }
       }
     }
     if (!team_reduce<1>(T, A.sync, A.partials, pq, red)) { err = SE_TIMEOUT; break; }
@@ -476,23 +570,24 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
 }
 
 template <typename K>
-int coop_blocks(Ctx* c, K kernel, int* blocks) {
+int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   int per_sm = 0;
-  FVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kSolverThreads, 0));
+  FVB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0));
   if (per_sm < 1) {
     fvb_set_error("solver kernel cannot be resident");
     return FVB_E_CUDA;
   }
-  if (per_sm > 2) per_sm = 2;
+  if (per_sm > max_per_sm) per_sm = max_per_sm;
   const int b = per_sm * c->num_sms / (c->sm_share > 0 ? c->sm_share : 1);
   *blocks = b < 1 ? 1 : b;
   return FVB_OK;
 }
 
 template <typename K, typename Args>
-int coop_launch(Ctx* c, K kernel, Args& args) {
+int coop_launch(Ctx* c, K kernel, Args& args, int threads = kSolverThreads, int max_per_sm = 2) {
+  const int kSolverThreads = threads;
   int blocks = 0;
-  FVB_TRY(coop_blocks(c, kernel, &blocks));
+  FVB_TRY(coop_blocks(c, kernel, threads, max_per_sm, &blocks));
   // words 0-2: arrivals, generation, abort; word 3 (team error) is sticky
   FVB_CUDA(cudaMemsetAsync(c->sync, 0, 3 * sizeof(unsigned), c->stream));
   void* params[] = {&args};
@@ -583,10 +678,32 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
                S_SCR + 2, S_SCR + 3, S_SCR + 4, tol, abs_tol, max_iters,
                c->sync, c->partials, result};
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
+  // FVB_CG_VARIANT selects an alternative kernel configuration (tuning
+  // experiments, tools/cg_micro.py); the default is the measured best:
+  // software-pipelined pass A with evict-first matrix loads, grid-strided
+  // rows, 2 x 512 threads per SM (profiles/r01_cg_variants.md).
+  static const int variant = [] {
+    const char* e = getenv("FVB_CG_VARIANT");
+    return e ? atoi(e) : -1;
+  }();
   switch (c->k) {
-    case 5: FVB_TRY(coop_launch(c, k_cg<5>, prm)); break;
-    case 7: FVB_TRY(coop_launch(c, k_cg<7>, prm)); break;
-    default: FVB_TRY(coop_launch(c, k_cg<0>, prm)); break;
+    case 5: FVB_TRY(coop_launch(c, k_cg<5, 512, 2, 2>, prm)); break;
+    case 7:
+      switch (variant) {
+        case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;
+        case 1: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 1>, prm, 512, 2)); break;
+        case 2: FVB_TRY(coop_launch(c, k_cg<7, 256, 3, 1>, prm, 256, 3)); break;
+        case 3: FVB_TRY(coop_launch(c, k_cg<7, 512, 1, 1>, prm, 512, 1)); break;
+        case 4: FVB_TRY(coop_launch(c, k_cg<7, 256, 4, 0>, prm, 256, 4)); break;
+        case 5: FVB_TRY(coop_launch(c, k_cg<7, 384, 2, 1>, prm, 384, 2)); break;
+        case 6: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 1, 1>, prm, 512, 2)); break;
+        case 7: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2, 1>, prm, 512, 2)); break;
+        case 8: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0, 1>, prm, 512, 2)); break;
+        case 10: FVB_TRY(coop_launch(c, k_cg<7, 256, 3, 2, 1>, prm, 256, 3)); break;
+        default: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;
+      }
+      break;
+    default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
   }
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[6];

@@ -22,6 +22,7 @@ and gather u, p, flux back into global order on request.
 """
 
 import ctypes as C
+import os
 import threading
 
 import numpy as np
@@ -316,10 +317,10 @@ class RankRun(_TeamRunBase):
         part, _ = slab_partition(mesh.n_cells, size)
         self.rank, self.nparts = rank, size
         sd = build_subdomain(mesh, self.pattern, part, rank)
-        self.member = _Member(sd, self.geom, mesh.n_internal, device, 1)
+        # FVB_SM_SHARE > 1: several ranks (processes) share one device (tests)
+        share = int(os.environ.get("FVB_SM_SHARE", "1"))
+        self.member = _Member(sd, self.geom, mesh.n_internal, device, share)
         base, nc, handle = self.member.export()
-        import os
-
         infos = allgather((os.getpid(), device, base, nc, handle))
         self._opened = []
         bases = []

@@ -1,0 +1,36 @@
+"""CG kernel microbenchmark: fixed-iteration Jacobi-PCG on a cavity
+Laplacian-like SPD matrix (K = 7) through fvb_op_cg; prints device time per
+iteration and the algorithmic HBM rate (N(12K+96) bytes per iteration).
+Usage: python tools/cg_micro.py N ITERS  (FVB_CG_VARIANT selects the kernel)"""
+import ctypes as C, json, os, sys, time
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import numpy as np
+from paper_1207_1571_b200 import _lib, cases, sparse
+from paper_1207_1571_b200.device import context_for
+
+n = int(sys.argv[1]); iters = int(sys.argv[2])
+t0 = time.time()
+mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
+pat = sparse.build_pattern(mesh)
+N, K = pat.n, pat.k
+V = np.where(pat.I >= 0, -1.0, 0.0)
+V[np.arange(N), pat.diag_slot] = (pat.I >= 0).sum(axis=1) - 1 + 0.01
+b = np.random.default_rng(0).normal(size=N)
+x = np.empty(N)
+ctx = context_for(None, None, pat)
+rep = _lib.SolveReportC()
+P = _lib.ptr
+crs = np.zeros(max(pat.nnz_crs, 1))
+setup = time.time() - t0
+res = []
+for rpt in range(3):
+    rc = _lib.lib.fvb_op_cg(ctx.h, P(_lib.f64(V)), P(crs), P(b), P(np.zeros(N)), P(x), 1e-300, 0.0,
+                            iters, C.byref(rep))
+    _lib.check(rc)
+    res.append(rep.wall_time)
+t = min(res)
+bytes_it = N * (12 * K + 96)
+setup_b = N * (12 * K + 80)
+print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "0"), "n": n, "iters": rep.iterations,
+                  "us_per_iter": 1e6 * t / iters,
+                  "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1)}))
