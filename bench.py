@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=["c2", "c5"])
-    ap.add_argument("--n", type=int, default=0, help="override cells per edge")
+    ap.add_argument("--edge", type=int, default=0, help="override cells per edge (not --n: torchrun prefix-matches it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cg-sample", type=int, default=20)
@@ -68,7 +68,7 @@ def parse():
 
 
 def workload(args):
-    return args.n or (128 if args.config == "c2" else 256)
+    return args.edge or (128 if args.config == "c2" else 256)
 
 
 def peaks():

@@ -146,6 +146,11 @@ typedef struct {
   double wall_time;   /* device time, seconds                        */
   int32_t error_iteration; /* >0 when the solve raised at that iteration */
   int32_t error_kind;      /* 0 none, see fvb.cu solver error table      */
+  /* device stage timers of the persistent kernel (seconds; StageTimer
+   * buckets of linsolve.py:18-79): SpMV passes (with the fused p-update /
+   * preconditioner), vector-update passes (with the fused z = r/D and the
+   * per-thread dot partials), and the grid/team reductions */
+  double t_smvp, t_daxpy, t_reduction;
 } fvb_solve_report;
 int fvb_op_cg(fvb_ctx* ctx, const double* V, const double* crs,
               const double* b, const double* x0, double* x, double tol,

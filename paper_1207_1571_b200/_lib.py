@@ -58,6 +58,9 @@ class SolveReportC(C.Structure):
         ("wall_time", C.c_double),
         ("error_iteration", C.c_int32),
         ("error_kind", C.c_int32),
+        ("t_smvp", C.c_double),
+        ("t_daxpy", C.c_double),
+        ("t_reduction", C.c_double),
     ]
 
 

@@ -32,7 +32,7 @@ from .fvm import (
     make_scalar,
     make_vector,
 )
-from .linsolve import SolveConfig, SolveReport
+from .linsolve import SolveConfig, SolveReport, stage_times_of
 from .mesh import compute_geometry
 from .sparse import build_pattern
 
@@ -327,13 +327,14 @@ def _run_device_step(state, cfg, piso):
         # (solver, iterations, device seconds of the persistent solver kernel)
         state._last_solves.append((solver, int(r.iterations), float(r.wall_time)))
         sc = cfg.pressure if solver == "cg" else cfg.momentum
-        st = {}
-        if sc.record_stages:
-            st = {s: 0.0 for s in ("smvp", "daxpy", "dot", "reduction", "precond")}
-            st["other"] = 0.0
+        # the 3 batched momentum solves share one kernel: its stage times are
+        # booked once (on ux)
+        shared = solver == "bicgstab" and rep.field[k] != 0
+        st = {} if shared else stage_times_of(r, sc.record_stages)
         state.log_solve(solver, _FIELD_NAMES[rep.field[k]],
                         SolveReport(int(r.iterations), float(r.initial_residual),
-                                    float(r.final_residual), bool(r.converged), 0.0, st))
+                                    float(r.final_residual), bool(r.converged),
+                                    float(r.wall_time), st))
     if rc != 0:
         msg = _lib.last_error().replace("{outer}", str(state.outer))
         if rc in (_lib.E_COUPLING,):

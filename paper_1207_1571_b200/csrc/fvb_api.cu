@@ -314,6 +314,9 @@ void fill_report(fvb_solve_report& r, const SolveOut& o) {
   r.wall_time = o.kernel_ms * 1e-3;
   r.error_iteration = o.error_iteration;
   r.error_kind = o.error_kind;
+  r.t_smvp = o.t_smvp;
+  r.t_daxpy = o.t_daxpy;
+  r.t_reduction = o.t_red;
 }
 
 int log_solve(fvb_step_report* rep, int solver, int field, const SolveOut& o) {

@@ -460,6 +460,7 @@ struct SolveOut {
   int iterations, converged, error_kind, error_iteration;
   double res0, res;
   double kernel_ms;  // device time of the persistent solver kernel alone
+  double t_smvp, t_daxpy, t_red;  // device stage timers (s), block 0's view
 };
 enum SolveErr {
   SE_NONE = 0,

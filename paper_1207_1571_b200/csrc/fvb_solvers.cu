@@ -183,8 +183,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   double* pnew = A.pb;
   int slot_new = A.slot_pb;
   bool first = true;
+  uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
+  const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
   while (!conv && it < A.max_iters) {
     ++it;
+    if (timer) tk = global_ns();
     // pass A: p <- z + beta p (gathered columns), q = A p, p.q
     double pq[1] = {0.0};
     {
@@ -205,7 +208,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
         }
       }
     }
+    if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
     if (!team_reduce<1>(T, A.sync, A.partials, pq, red)) { err = SE_TIMEOUT; break; }
+    if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
     // pass B: x += alpha p, r -= alpha q, z = r / D, ||r||^2, r.z
@@ -221,7 +226,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s2[0] += ri * ri;
       s2[1] += ri * zi;
     }
+    if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
     if (!team_reduce<2>(T, A.sync, A.partials, s2, red)) { err = SE_TIMEOUT; break; }
+    if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
     if (res <= A.tol || res * bnorm <= A.abs_tol) { conv = true; break; }
@@ -238,6 +245,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     A.result[3] = res;
     A.result[4] = err;
     A.result[5] = err ? it : 0;
+    A.result[6] = 1e-9 * double(t_spmv);
+    A.result[7] = 1e-9 * double(t_axpy);
+    A.result[8] = 1e-9 * double(t_red);
   }
 }
 
@@ -375,7 +385,10 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
   }
   __syncthreads();
 
+  uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
+  const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
   while (!timeout) {
+    if (timer) tk = global_ns();
     // per-component scalar logic (linsolve.py:198-219), identical in every block
     if (threadIdx.x == 0) {
       for (int c = 0; c < NC; ++c) {
@@ -427,10 +440,12 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
         if (S[c].restart) A.rh[c][i] = ri;
       }
     }
+    if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
     {
       double z1[1] = {0.0};
       if (!team_reduce<1>(T, A.sync, A.partials, z1, red)) { timeout = true; break; }
     }
+    if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
     // pass V: v = A p_hat, r_hat.v
     {
       double rv[NC];
@@ -447,7 +462,9 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
           rv[c] += A.rh[c][i] * y[c];
         }
       }
+      if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
       if (!team_reduce<NC>(T, A.sync, A.partials, rv, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
@@ -477,7 +494,9 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
           ss[c] += si * si;
         }
       }
+      if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
       if (!team_reduce<NC>(T, A.sync, A.partials, ss, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
@@ -512,7 +531,9 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
           tts[2 * c + 1] += y[c] * A.s[c][i];
         }
       }
+      if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
       if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
@@ -544,7 +565,9 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
           rr[2 * c + 1] += A.rh[c][i] * ri;
         }
       }
+      if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
       if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
           if (!tact[c]) continue;
@@ -566,6 +589,9 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
       A.result[6 * c + 4] = timeout ? SE_TIMEOUT : S[c].err;
       A.result[6 * c + 5] = S[c].err_it;
     }
+    A.result[18] = 1e-9 * double(t_spmv);
+    A.result[19] = 1e-9 * double(t_axpy);
+    A.result[20] = 1e-9 * double(t_red);
   }
 }
 
@@ -668,7 +694,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
   FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
-  *out = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0};
+  *out = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (zero_row != 0x7fffffff) {
     out->error_kind = SE_ZERO_DIAG;
     out->error_iteration = zero_row;
@@ -706,7 +732,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
     default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
   }
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
-  double h[6];
+  double h[9];
   unsigned team_err = 0;
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof h, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaMemcpyAsync(&team_err, c->sync + 3, sizeof team_err, cudaMemcpyDeviceToHost, c->stream));
@@ -718,6 +744,9 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   out->res = h[3];
   out->error_kind = int(h[4]);
   out->error_iteration = int(h[5]);
+  out->t_smvp = h[6];
+  out->t_daxpy = h[7];
+  out->t_red = h[8];
   float kms = 0.f;
   FVB_CUDA(cudaEventElapsedTime(&kms, c->kev[0], c->kev[1]));
   out->kernel_ms = kms;
@@ -767,7 +796,7 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
   FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
-  for (int k = 0; k < ncomp; ++k) out[k] = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < ncomp; ++k) out[k] = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (zero_row != 0x7fffffff) {
     out[0].error_kind = SE_ZERO_DIAG;
     out[0].error_iteration = zero_row;
@@ -783,10 +812,9 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
   else
     FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
-  double h[18];
+  double h[21];
   unsigned team_err = 0;
-  FVB_CUDA(cudaMemcpyAsync(h, result, sizeof(double) * 6 * ncomp, cudaMemcpyDeviceToHost,
-                           c->stream));
+  FVB_CUDA(cudaMemcpyAsync(h, result, sizeof(double) * 21, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaMemcpyAsync(&team_err, c->sync + 3, sizeof team_err, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
   if (team_err)
@@ -798,6 +826,9 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
     out[k].res = h[6 * k + 3];
     out[k].error_kind = int(h[6 * k + 4]);
     out[k].error_iteration = int(h[6 * k + 5]);
+    out[k].t_smvp = h[18];
+    out[k].t_daxpy = h[19];
+    out[k].t_red = h[20];
   }
   float kms = 0.f;
   FVB_CUDA(cudaEventElapsedTime(&kms, c->kev[0], c->kev[1]));

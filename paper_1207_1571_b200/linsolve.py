@@ -48,20 +48,25 @@ class SolveReport:
     stage_times: dict = field(default_factory=dict)
 
 
-def _stage_times(cfg, wall):
-    # the fused device kernel cannot split its time by kernel group; the
-    # whole device time is reported under "other" (linsolve.py:73-79)
-    if not cfg.record_stages:
+def stage_times_of(r, record):
+    """StageTimer buckets (linsolve.py:18-79) from the persistent kernel's
+    device timers: the SpMV passes carry the fused p-update/preconditioner,
+    the vector passes carry z = r/D and the dot partials, the grid/team
+    reductions are "reduction"; setup and launch are the "other" remainder."""
+    if not record:
         return {}
     d = dict.fromkeys(STAGES, 0.0)
-    d["other"] = wall
+    d["smvp"] = float(r.t_smvp)
+    d["daxpy"] = float(r.t_daxpy)
+    d["reduction"] = float(r.t_reduction)
+    d["other"] = max(float(r.wall_time) - d["smvp"] - d["daxpy"] - d["reduction"], 0.0)
     return d
 
 
 def _report(r, cfg):
     return SolveReport(iterations=int(r.iterations), initial_residual=float(r.initial_residual),
                        final_residual=float(r.final_residual), converged=bool(r.converged),
-                       wall_time=float(r.wall_time), stage_times=_stage_times(cfg, r.wall_time))
+                       wall_time=float(r.wall_time), stage_times=stage_times_of(r, cfg.record_stages))
 
 
 def _solve(fn, A, b, x0, cfg, ncomp=1):

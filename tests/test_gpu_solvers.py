@@ -123,3 +123,23 @@ def test_error_contract():
 
 def random_spd_hybrid(n):
     return hybrid_from_dense(random_spd(np.random.default_rng(1), n))
+
+
+def test_stage_times_from_device_timers():
+    """record_stages fills the reference's six StageTimer buckets
+    (linsolve.py:18-79) from the persistent kernel's device timers."""
+    from paper_1207_1571_b200.linsolve import STAGES
+
+    case, g = golden_case("cav6")
+    pat = sparse.build_pattern(case.mesh)
+    n = case.mesh.n_cells
+    A = sparse.HybridMatrix.zeros(pat)
+    A.V[:] = g["sol_cg_V"]
+    x, rep = cg(A, g["in_b"], np.zeros(n), SolveConfig(tolerance=1e-10, max_iters=5000,
+                                                       record_stages=True))
+    st = rep.stage_times
+    assert set(st) == set(STAGES)
+    assert st["smvp"] > 0 and st["daxpy"] > 0 and st["reduction"] > 0
+    assert sum(st.values()) <= rep.wall_time * 1.000001 + 1e-9
+    x, rep = cg(A, g["in_b"], np.zeros(n), SolveConfig(tolerance=1e-10, max_iters=5000))
+    assert rep.stage_times == {}

@@ -92,3 +92,34 @@ def test_team_cavity24_four_ranks():
         assert abs(a[3] - b[3]) <= (1 if a[0] == "cg" else 2), (a, b)
     assert continuity_error(st) <= 1e-8 * np.abs(st.flux).max()
     run.close()
+
+
+def test_ipc_team_two_processes_one_device():
+    """The one-process-per-GPU path (RankRun: CUDA IPC pool mappings,
+    torch.distributed plumbing) with both ranks on this device."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, FVB_DEVICE="0", FVB_SM_SHARE="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(here, "tools", "ipc_team_check.py"), "8"]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300, cwd=here)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = [ln for ln in out.stdout.splitlines() if ln.startswith("IPC team of 2")]
+    assert line, out.stdout[-2000:]
+    import re
+
+    rels = [float(x) for x in re.findall(r"(?:u|p|flux) ([0-9.e+-]+)", line[0])]
+    assert len(rels) == 3 and max(rels) < 1e-9, line[0]
+    team, single = re.findall(r"\[([0-9, ]+)\]", line[0])
+    ta = [int(x) for x in team.split(",")]
+    sa = [int(x) for x in single.split(",")]
+    assert len(ta) == len(sa) and all(abs(a - b) <= 1 for a, b in zip(ta, sa)), line[0]
