@@ -501,6 +501,11 @@ def run_ours(args):
                      "bytes_per_step": step_bytes / args.steps},
         "iterations_per_step": {"cg": sum(cg_iters) / args.steps,
                                 "bicgstab": sum(bi_iters) / args.steps},
+        "kernel_ms_per_step": {
+            "k_cg": 1e3 * D.max(sum(ks for sv, _, ks in kernel_rows if sv == "cg")) / args.steps,
+            # the 3 batched momentum solves share one launch (its time is on each row)
+            "k_bicgstab": 1e3 * D.max(sum(ks for sv, _, ks in kernel_rows if sv == "bicgstab"))
+            / 3 / args.steps},
         "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,

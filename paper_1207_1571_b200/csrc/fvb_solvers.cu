@@ -61,6 +61,73 @@ __device__ __forceinline__ T ld_mat(const T* p) {
   return __ldg(p);
 }
 
+// Variant of the pipelined pass A that prefetches only the column indices
+// (the gather's address chain) DEPTH rows ahead; the values V of the current
+// row are loaded in-iteration (they are off the critical path).
+template <int KT, int DEPTH, bool HINT>
+__device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const double* __restrict__ z,
+                                                  const double* __restrict__ po,
+                                                  double* __restrict__ pnew, double beta,
+                                                  bool first, int slot_new, int i, int end,
+                                                  int step) {
+  const PatternView& P = A.P;
+  const TeamView& T = A.T;
+  const int n = P.n;
+  const int* __restrict__ I = P.I;
+  const double* __restrict__ V = A.V;
+  const bool team = T.size > 1;
+  double acc = 0.0;
+  int cq[DEPTH][KT];
+#pragma unroll
+  for (int d = 0; d < DEPTH; ++d) {
+    const int r = i + d * step;
+    if (r < end) {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) cq[d][s] = __ldcs(I + size_t(s) * n + r);
+    }
+  }
+  auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
+  while (i < end) {
+    double vi[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) vi[s] = __ldcs(V + size_t(s) * n + i);
+    int ci[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) ci[s] = cq[0][s];
+#pragma unroll
+    for (int d = 0; d + 1 < DEPTH; ++d)
+#pragma unroll
+      for (int s = 0; s < KT; ++s) cq[d][s] = cq[d + 1][s];
+    const int nx = i + DEPTH * step;
+    if (nx < end) {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) cq[DEPTH - 1][s] = __ldcs(I + size_t(s) * n + nx);
+    }
+    double pr[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * g(ci[s] < 0 ? 0 : ci[s]);
+    double ev = pr[0];
+#pragma unroll
+    for (int s = 2; s < KT; s += 2) ev = ev + pr[s];
+    double y = ev;
+    if (KT > 1) {
+      double od = pr[1];
+#pragma unroll
+      for (int s = 3; s < KT; s += 2) od = od + pr[s];
+      y = ev + od;
+    }
+    const double qi = crs_tail(P, A.crs, i, y, g);
+    const double pi = g(i);
+    pnew[i] = pi;
+    A.q[i] = qi;
+    if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
+    acc += pi * qi;
+    i += step;
+  }
+  (void)HINT;
+  return acc;
+}
+
 template <int KT, bool STREAM>
 __device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double* __restrict__ z,
                                                  const double* __restrict__ po,
@@ -193,7 +260,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
-      if (PIPE && KT > 0) {
+      if (PIPE >= 3 && KT > 0) {
+        pq[0] = cg_pass_a_icols<(KT > 0 ? KT : 1), (PIPE >= 4 ? PIPE - 2 : 1), false>(
+            A, z, po, pnew, beta, first, slot_new, tid, n, G);
+      } else if (PIPE && KT > 0) {
         pq[0] = cg_pass_a_pipe<(KT > 0 ? KT : 1), (PIPE > 1)>(A, z, po, pnew, beta, first,
                                                                 slot_new, tid, n, G);
       } else {
@@ -320,6 +390,64 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
       yy = yy + tl;
     }
     y[c] = yy;
+  }
+}
+
+// Row sweep computing y_c = (A x_c)_i for the active components with the
+// column indices prefetched two rows ahead (the gather's address chain; see
+// cg_pass_a_icols) and evict-first matrix loads; body(i, y) consumes a row.
+// Same products and summation order as ell_rows_multi.
+template <int KT, int NC, typename Gt, typename Bt>
+__device__ __forceinline__ void spmv_sweep(const PatternView& P, const double* __restrict__ V,
+                                           const double* crs, int i, int end, int step,
+                                           const bool* act, Gt gather, Bt body) {
+  const int n = P.n;
+  int c0[KT], c1[KT];
+  if (i < end) {
+#pragma unroll
+    for (int s = 0; s < KT; ++s) c0[s] = __ldcs(P.I + size_t(s) * n + i);
+  }
+  if (i + step < end) {
+#pragma unroll
+    for (int s = 0; s < KT; ++s) c1[s] = __ldcs(P.I + size_t(s) * n + i + step);
+  }
+  while (i < end) {
+    double v[KT];
+    int ci[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) {
+      v[s] = __ldcs(V + size_t(s) * n + i);
+      ci[s] = c0[s] < 0 ? 0 : c0[s];
+      c0[s] = c1[s];
+    }
+    const int nx = i + 2 * step;
+    if (nx < end) {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) c1[s] = __ldcs(P.I + size_t(s) * n + nx);
+    }
+    double y[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      if (!act[c]) continue;
+      double ev = v[0] * gather(c, ci[0]);
+#pragma unroll
+      for (int s = 2; s < KT; s += 2) ev = ev + v[s] * gather(c, ci[s]);
+      double yy = ev;
+      if (KT > 1) {
+        double od = v[1] * gather(c, ci[1]);
+#pragma unroll
+        for (int s = 3; s < KT; s += 2) od = od + v[s] * gather(c, ci[s]);
+        yy = ev + od;
+      }
+      if (P.nnz_crs) {
+        double tl = 0.0;
+        for (int q = P.crs_ptr[i]; q < P.crs_ptr[i + 1]; ++q) tl += crs[q] * gather(c, P.crs_col[q]);
+        yy = yy + tl;
+      }
+      y[c] = yy;
+    }
+    body(i, y);
+    i += step;
   }
 }
 
@@ -451,15 +579,22 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
       double rv[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) rv[c] = 0.0;
-      for (int i = tid; i < n; i += G) {
-        double y[NC];
-        auto g = [&](int c, int col) { return A.ph[c][col]; };
-        ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
+      auto g = [&](int c, int col) { return A.ph[c][col]; };
+      auto body = [&](int i, const double* y) {
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
           A.v[c][i] = y[c];
           rv[c] += A.rh[c][i] * y[c];
+        }
+      };
+      if (KT > 0) {
+        spmv_sweep<(KT > 0 ? KT : 1), NC>(P, A.V, A.crs, tid, n, G, act, g, body);
+      } else {
+        for (int i = tid; i < n; i += G) {
+          double y[NC];
+          ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
+          body(i, y);
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
@@ -516,19 +651,29 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) 
       double tts[2 * NC];
 #pragma unroll
       for (int m = 0; m < 2 * NC; ++m) tts[m] = 0.0;
-      for (int i = tid; i < n; i += G) {
+      auto g = [&](int c, int col) { return A.sh[c][col]; };
+      auto body = [&](int i, const double* y) {
 #pragma unroll
         for (int c = 0; c < NC; ++c)
           if (act[c] && S[c].sconv) A.x[c][i] = A.x[c][i] + S[c].alpha * A.ph[c][i];
-        double y[NC];
-        auto g = [&](int c, int col) { return A.sh[c][col]; };
-        ell_rows_multi<KT, NC>(P, A.V, A.crs, i, tact, g, y);
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           if (!tact[c]) continue;
           A.t[c][i] = y[c];
           tts[2 * c] += y[c] * y[c];
           tts[2 * c + 1] += y[c] * A.s[c][i];
+        }
+      };
+      bool any_t = false;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) any_t = any_t || tact[c];
+      if (KT > 0 && any_t) {
+        spmv_sweep<(KT > 0 ? KT : 1), NC>(P, A.V, A.crs, tid, n, G, tact, g, body);
+      } else {
+        for (int i = tid; i < n; i += G) {
+          double y[NC];
+          ell_rows_multi<KT, NC>(P, A.V, A.crs, i, tact, g, y);
+          body(i, y);
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
@@ -706,14 +851,15 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
   // FVB_CG_VARIANT selects an alternative kernel configuration (tuning
   // experiments, tools/cg_micro.py); the default is the measured best:
-  // software-pipelined pass A with evict-first matrix loads, grid-strided
-  // rows, 2 x 512 threads per SM (profiles/r01_cg_variants.md).
+  // pass A with the column indices prefetched two rows ahead (the gather's
+  // address chain), evict-first matrix loads, grid-strided rows, 2 x 512
+  // threads per SM (profiles/r01_cg_variants.md).
   static const int variant = [] {
     const char* e = getenv("FVB_CG_VARIANT");
     return e ? atoi(e) : -1;
   }();
   switch (c->k) {
-    case 5: FVB_TRY(coop_launch(c, k_cg<5, 512, 2, 2>, prm)); break;
+    case 5: FVB_TRY(coop_launch(c, k_cg<5, 512, 2, 4>, prm)); break;
     case 7:
       switch (variant) {
         case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;
@@ -726,7 +872,14 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
         case 7: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2, 1>, prm, 512, 2)); break;
         case 8: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0, 1>, prm, 512, 2)); break;
         case 10: FVB_TRY(coop_launch(c, k_cg<7, 256, 3, 2, 1>, prm, 256, 3)); break;
-        default: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;
+        case 11: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 3>, prm)); break;
+        case 12: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;
+        case 13: FVB_TRY(coop_launch(c, k_cg<7, 384, 2, 4>, prm, 384, 2)); break;
+        case 14: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 5>, prm)); break;
+        case 15: FVB_TRY(coop_launch(c, k_cg<7, 256, 4, 4>, prm, 256, 4)); break;
+        case 16: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 6>, prm)); break;
+        case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;
+        default: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;
       }
       break;
     default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
