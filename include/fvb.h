@@ -38,6 +38,8 @@ extern "C" {
 #define FVB_E_COUPLING -6   /* coupling.CouplingError    (coupling.py:64)      */
 #define FVB_E_CUDA -7       /* device / driver failure                          */
 #define FVB_E_TIMEOUT -8    /* device watchdog fired inside a persistent kernel */
+#define FVB_E_MESHFILE -9   /* fileio.MeshFileError      (fileio.py:27)        */
+#define FVB_E_IO -10        /* OSError opening / writing a file                 */
 
 /* boundary-condition kinds per boundary face (fvm.py:37-105) */
 #define FVB_BC_ZERO_GRADIENT 0
@@ -81,6 +83,27 @@ int fvb_pattern_plan_fill(fvb_pattern_plan* plan, int64_t n_face_pairs,
                           uint8_t* crs_twin_in_ell, int64_t* crs_twin_pos,
                           int64_t* face_addr);
 void fvb_pattern_plan_destroy(fvb_pattern_plan* plan);
+
+/* Mesh file I/O (fileio.py:50-185): the reference's ASCII format, read
+ * with its exact line-numbered MeshFileError messages and written with
+ * "%.17g" so files are byte-identical to fvflow's.  Read is two-phase:
+ * fvb_mesh_read parses and returns counts[5] = {n_points, n_faces,
+ * n_face_points, n_internal, n_patches}; fvb_mesh_read_take copies into
+ * caller arrays (names/kinds: n_patches x 256 chars) and keeps the handle
+ * valid until fvb_mesh_read_free. */
+typedef struct fvb_meshfile fvb_meshfile;
+int fvb_mesh_read(const char* path, fvb_meshfile** out, int64_t* counts);
+int fvb_mesh_read_take(fvb_meshfile* mf, double* points, int64_t* face_offsets,
+                       int64_t* face_points, int64_t* owner, int64_t* neighbour,
+                       int64_t* patch_start, int64_t* patch_count, char* patch_names,
+                       char* patch_kinds);
+void fvb_mesh_read_free(fvb_meshfile* mf);
+int fvb_mesh_write(const char* path, int64_t n_points, const double* points,
+                   int64_t n_faces, const int64_t* face_offsets,
+                   const int64_t* face_points, const int64_t* owner,
+                   int64_t n_internal, const int64_t* neighbour, int64_t n_patches,
+                   const char* const* names, const char* const* kinds,
+                   const int64_t* start, const int64_t* count);
 
 /* ---------------------------------------------------------------- context */
 int fvb_ctx_create(int device, fvb_ctx** out);
@@ -137,6 +160,19 @@ int fvb_get_state(fvb_ctx* ctx, double* u, double* p, double* flux,
 /* smvp (sparse.py:296-305) */
 int fvb_op_smvp(fvb_ctx* ctx, const double* V, const double* crs,
                 const double* x, double* y);
+/* stmvp (sparse.py:308-334): y = A^T x without forming the transpose,
+ * twins through J (row-major (n,k) ELL twin slots), ell_twin_crs (CRS
+ * position of an ELL entry's twin) and the CRS back-references */
+int fvb_op_stmvp(fvb_ctx* ctx, const double* V, const double* crs, const int64_t* J,
+                 const int64_t* ell_twin_crs, const uint8_t* crs_twin_in_ell,
+                 const int64_t* crs_twin_row, const int64_t* crs_twin_pos,
+                 const double* x, double* y);
+/* pack_q / unpack_q (sparse.py:337-363), host-side: mode 0 by_N, 1 by_K;
+ * I, J, q are (n*k) row-major; unpack_q decodes m entries */
+int fvb_pack_q(int64_t n, int64_t k, const int64_t* I, const int64_t* J, int mode,
+               int64_t* q);
+int fvb_unpack_q(int64_t n, int64_t k, int64_t m, const int64_t* q, int mode,
+                 int64_t* I, int64_t* J);
 /* cg (linsolve.py:102-172) / bicgstab (linsolve.py:175-282) */
 typedef struct {
   int32_t iterations;
@@ -228,6 +264,12 @@ typedef struct {
   double t_momentum_assembly, t_momentum_solve, t_pressure_assembly,
       t_pressure_solve, t_correction;
   int32_t failed_solve;             /* index of the solve that raised, -1 */
+  /* per-operator device times and call counts, RunState.ops keys
+   * (coupling.py:166, 223-229, 252, 299, 313, 340), in the order
+   * ddt, convection, laplacian, gradient, divergence; a laplacian includes
+   * its non-orthogonal-correction gradient as in the reference */
+  double op_seconds[5];
+  int32_t op_calls[5];
 } fvb_step_report;
 
 /* piso_time_step (coupling.py:356-370) with speeds[] for time-dependent

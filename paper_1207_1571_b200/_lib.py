@@ -16,6 +16,7 @@ from .errors import (
     DeviceError,
     FvmError,
     MeshError,
+    MeshFileError,
     SolverError,
     SparseError,
 )
@@ -30,7 +31,8 @@ lib = C.CDLL(LIB_PATH)
 
 BC_ZERO_GRADIENT, BC_EMPTY, BC_FIXED, BC_NO_SLIP, BC_SINE, BC_MASS_FLOW = range(6)
 
-E_ARG, E_MESH, E_SPARSE, E_SOLVER, E_FVM, E_COUPLING, E_CUDA, E_TIMEOUT = range(-1, -9, -1)
+E_ARG, E_MESH, E_SPARSE, E_SOLVER, E_FVM, E_COUPLING, E_CUDA, E_TIMEOUT, E_MESHFILE, E_IO = range(
+    -1, -11, -1)
 _ERR = {
     E_ARG: ValueError,
     E_MESH: MeshError,
@@ -40,6 +42,8 @@ _ERR = {
     E_COUPLING: CouplingError,
     E_CUDA: DeviceError,
     E_TIMEOUT: DeviceError,
+    E_MESHFILE: MeshFileError,
+    E_IO: OSError,
 }
 
 dp = C.POINTER(C.c_double)
@@ -107,6 +111,8 @@ class StepReportC(C.Structure):
         ("t_pressure_solve", C.c_double),
         ("t_correction", C.c_double),
         ("failed_solve", C.c_int32),
+        ("op_seconds", C.c_double * 5),
+        ("op_calls", C.c_int32 * 5),
     ]
 
 
@@ -129,6 +135,11 @@ _sig("fvb_pattern_plan_create", I, I64, I64, i64p, I64, C.POINTER(vp), i64p, i64
 _sig("fvb_pattern_plan_fill", I, vp, I64, i64p, i64p, i64p, i64p, i64p, i64p, i64p,
      u8p, i64p, i64p)
 _sig("fvb_pattern_plan_destroy", None, vp)
+_sig("fvb_mesh_read", I, C.c_char_p, C.POINTER(vp), i64p)
+_sig("fvb_mesh_read_take", I, vp, dp, i64p, i64p, i64p, i64p, i64p, i64p, C.c_char_p, C.c_char_p)
+_sig("fvb_mesh_read_free", None, vp)
+_sig("fvb_mesh_write", I, C.c_char_p, I64, dp, I64, i64p, i64p, i64p, I64, i64p, I64,
+     C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), i64p, i64p)
 _sig("fvb_ctx_create", I, I, C.POINTER(vp))
 _sig("fvb_ctx_destroy", I, vp)
 _sig("fvb_ctx_device_bytes", I64, vp)
@@ -146,6 +157,9 @@ _sig("fvb_set_bcs", I, vp, I, u8p, i32p, dp, I)
 _sig("fvb_set_state", I, vp, dp, dp, dp, dp, dp)
 _sig("fvb_get_state", I, vp, dp, dp, dp, dp, dp)
 _sig("fvb_op_smvp", I, vp, dp, dp, dp, dp)
+_sig("fvb_op_stmvp", I, vp, dp, dp, i64p, i64p, u8p, i64p, i64p, dp, dp)
+_sig("fvb_pack_q", I, I64, I64, i64p, i64p, I, i64p)
+_sig("fvb_unpack_q", I, I64, I64, I64, i64p, I, i64p, i64p)
 _sig("fvb_op_cg", I, vp, dp, dp, dp, dp, dp, D, D, I, C.POINTER(SolveReportC))
 _sig("fvb_op_bicgstab", I, vp, dp, dp, dp, dp, dp, D, D, I, C.POINTER(SolveReportC))
 _sig("fvb_op_bicgstab_batched", I, vp, I, dp, dp, dp, dp, dp, D, D, I, C.POINTER(SolveReportC))
@@ -177,6 +191,8 @@ EXPORTS = [
     "fvb_upload_mesh_part", "fvb_team_export", "fvb_ipc_open", "fvb_ipc_close",
     "fvb_team_attach", "fvb_team_check", "fvb_team_allreduce", "fvb_set_sm_share",
     "fvb_upload_pattern", "fvb_set_bcs", "fvb_set_state", "fvb_get_state", "fvb_op_smvp",
+    "fvb_op_stmvp", "fvb_pack_q", "fvb_unpack_q",
+    "fvb_mesh_read", "fvb_mesh_read_take", "fvb_mesh_read_free", "fvb_mesh_write",
     "fvb_op_cg", "fvb_op_bicgstab", "fvb_op_bicgstab_batched", "fvb_op_apply_bcs",
     "fvb_op_interpolate", "fvb_op_gradient", "fvb_op_divergence", "fvb_op_laplacian",
     "fvb_op_laplacian_flux", "fvb_op_convection", "fvb_op_ddt", "fvb_piso_step",

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfvb.so")
-SOURCES = ["setup.cpp", "fvb_ops.cu", "fvb_solvers.cu", "fvb_team.cu", "fvb_api.cu"]
+SOURCES = ["setup.cpp", "meshio.cpp", "fvb_ops.cu", "fvb_solvers.cu", "fvb_team.cu", "fvb_api.cu"]
 HEADERS = ["common.h", "fvb_internal.cuh", os.path.join("..", "..", "include", "fvb.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -309,6 +309,7 @@ def _step_cfg(state, cfg):
 
 
 _FIELD_NAMES = ("ux", "uy", "uz", "p")
+_OP_NAMES = ("ddt", "convection", "laplacian", "gradient", "divergence")  # fvb_step_report order
 
 
 def _run_device_step(state, cfg, piso):
@@ -345,6 +346,11 @@ def _run_device_step(state, cfg, piso):
     state.add_wall("pressure_assembly", rep.t_pressure_assembly)
     state.add_wall("pressure_solve", rep.t_pressure_solve)
     state.add_wall("correction", rep.t_correction)
+    for i, name in enumerate(_OP_NAMES):
+        if rep.op_calls[i]:
+            rec = state.ops.setdefault(name, [0.0, 0])
+            rec[0] += float(rep.op_seconds[i])
+            rec[1] += int(rep.op_calls[i])
     state._last_step_s = time.perf_counter() - t0
     return float(rep.mom_res), float(rep.p_res)
 

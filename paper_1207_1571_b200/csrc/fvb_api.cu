@@ -337,6 +337,29 @@ float ev_ms(Ctx* c, int a, int b) {
   return ms;
 }
 
+// RunState.ops timing: an event pair around each operator of the step
+enum OpId { OP_DDT = 0, OP_CONV = 1, OP_LAP = 2, OP_GRAD = 3, OP_DIV = 4 };
+
+int op_begin(Ctx* c, int op) {
+  if (c->n_op >= Ctx::kOpEvents / 2) return -1;
+  const int k = c->n_op++;
+  c->op_id[k] = op;
+  cudaEventRecord(c->opev[2 * k], c->stream);
+  return k;
+}
+void op_end(Ctx* c, int k) {
+  if (k >= 0) cudaEventRecord(c->opev[2 * k + 1], c->stream);
+}
+void op_collect(Ctx* c, fvb_step_report* rep) {
+  for (int k = 0; k < c->n_op; ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->opev[2 * k], c->opev[2 * k + 1]);
+    rep->op_seconds[c->op_id[k]] += 1e-3 * ms;
+    rep->op_calls[c->op_id[k]] += 1;
+  }
+  c->n_op = 0;
+}
+
 // _momentum_matrix (coupling.py:216-231)
 int momentum_matrix(Ctx* c, const fvb_step_cfg* cfg, bool with_ddt) {
   StepWork w = work_of(c);
@@ -347,8 +370,15 @@ int momentum_matrix(Ctx* c, const fvb_step_cfg* cfg, bool with_ddt) {
   FVB_CUDA(cudaMemsetAsync(w.Vm, 0, sizeof(double) * c->k * n, c->stream));
   if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsm, 0, sizeof(double) * c->nnz_crs, c->stream));
   FVB_CUDA(cudaMemsetAsync(b0, 0, sizeof(double) * 3 * size_t(c->nc), c->stream));
-  if (with_ddt) FVB_TRY(op_ddt(c, 3, Am, b0, c->u, cfg->dt, 1.0));
+  if (with_ddt) {
+    const int t = op_begin(c, OP_DDT);
+    FVB_TRY(op_ddt(c, 3, Am, b0, c->u, cfg->dt, 1.0));
+    op_end(c, t);
+  }
+  int t = op_begin(c, OP_CONV);
   FVB_TRY(op_convection(c, 0, 3, Am, b0, c->flux, c->ub, cfg->scheme, 1.0));
+  op_end(c, t);
+  t = op_begin(c, OP_LAP);
   const bool corr = cfg->nonorth_correction && cfg->limiter > 0.0;
   if (corr) {
     FVB_TRY(op_gradient(c, 0, 3, c->u, c->ub, gu));
@@ -356,6 +386,7 @@ int momentum_matrix(Ctx* c, const fvb_step_cfg* cfg, bool with_ddt) {
   }
   FVB_TRY(op_laplacian(c, 0, 3, Am, b0, cfg->nu, nullptr, c->u, c->ub, gu,
                        cfg->nonorth_correction, cfg->limiter, -1.0, nullptr, nullptr));
+  op_end(c, t);
   return FVB_OK;
 }
 
@@ -369,7 +400,9 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   double* gp = c->slot(S_GP);
   double* rhs = c->slot(S_RHS);
   { k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, diag); fvb::note_launch(); }
+  const int tg = op_begin(c, OP_GRAD);
   FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+  op_end(c, tg);
   const bool relaxing = relax && cfg->alpha_u < 1.0;
   { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, nv, c->slot(S_B0), c->vol, gp, diag, c->u, rhs,
                                            w.Vm, c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
@@ -433,7 +466,9 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(team_halo(c, S_HV, 4));  // HbyA and rAU on processor faces
   FVB_TRY(op_face_flux(c, 3, hv, c->ub, 0, w.phih));
+  const int td = op_begin(c, OP_DIV);
   FVB_TRY(op_divergence(c, w.phih, divh));
+  op_end(c, td);
   FVB_TRY(op_interp(c, -1, 1, rau, nullptr, w.rauf));
   if (relax_p) FVB_CUDA(cudaMemcpyAsync(pbefore, c->p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c->stream));
   FVB_CUDA(cudaEventRecord(c->ev[5], c->stream));
@@ -445,12 +480,14 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
     FVB_CUDA(cudaMemsetAsync(w.Vp, 0, sizeof(double) * c->k * size_t(n), c->stream));
     if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsp, 0, sizeof(double) * c->nnz_crs, c->stream));
     FVB_CUDA(cudaMemsetAsync(rl, 0, sizeof(double) * nv, c->stream));
+    const int tl = op_begin(c, OP_LAP);
     if (corr) {
       FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
       FVB_TRY(team_halo(c, S_GP, 3));
     }
     FVB_TRY(op_laplacian(c, 1, 1, Ap, rl, 0.0, w.rauf, c->p, c->pb, gp,
                          cfg->nonorth_correction, cfg->limiter, -1.0, w.coef, w.corr));
+    op_end(c, tl);
     { k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, rl, divh, rp); fvb::note_launch(); }
     if (cfg->pin_pressure)
       { k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, rp, cfg->pressure_ref_cell,
@@ -485,7 +522,9 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
   }
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
+  const int tg = op_begin(c, OP_GRAD);
   FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+  op_end(c, tg);
   { k_u_corr<<<g, kThreads, 0, c->stream>>>(n, nv, hv, rau, gp, c->u); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(team_halo(c, S_U, 3));
@@ -506,6 +545,7 @@ int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_rep
   FVB_TRY(need_bc(c, 1));
   FVB_TRY(ensure_work(c));
   memset(rep, 0, sizeof(*rep));
+  c->n_op = 0;
   rep->failed_solve = -1;
   rep->p_res = -1.0;
   if (c->n_patches[0] && speeds)
@@ -527,6 +567,8 @@ int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_rep
     FVB_TRY(pressure_correct(c, cfg, !piso, rep, &first, &rep->t_pressure_assembly,
                              &rep->t_pressure_solve, &rep->t_correction));
   rep->p_res = first;
+  FVB_CUDA(cudaStreamSynchronize(c->stream));
+  op_collect(c, rep);
   if (c->teamed()) {
     unsigned err = 0;
     FVB_CUDA(cudaMemcpyAsync(&err, c->sync + 3, sizeof err, cudaMemcpyDeviceToHost, c->stream));
@@ -571,6 +613,7 @@ int fvb_ctx_create(int device, fvb_ctx** out) {
   for (auto& ev : c->ev) cudaEventCreate(&ev);
   for (auto& ev : c->tev) cudaEventCreate(&ev);
   for (auto& ev : c->kev) cudaEventCreate(&ev);
+  for (auto& ev : c->opev) cudaEventCreate(&ev);
   int rc = dalloc(c, &c->sync, 64);
   if (!rc) rc = dalloc(c, &c->partials, 16 * 4096 + 256);
   if (!rc) rc = dalloc(c, &c->ipart, 64);
@@ -594,6 +637,8 @@ int fvb_ctx_destroy(fvb_ctx* h) {
   for (auto& ev : c->tev)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : c->kev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : c->opev)
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   drop_ext(c);
@@ -906,6 +951,45 @@ int fvb_op_smvp(fvb_ctx* h, const double* V, const double* crs, const double* x,
   FVB_TRY(tmp_zero(c, ty, c->nc, &dy));
   FVB_TRY(smvp(c, M.m, dx, dy));
   FVB_TRY(d2h(c, y, dy, c->nc));
+  return sync(c);
+}
+
+int fvb_op_stmvp(fvb_ctx* h, const double* V, const double* crs, const int64_t* J,
+                 const int64_t* ell_twin_crs, const uint8_t* crs_twin_in_ell,
+                 const int64_t* crs_twin_row, const int64_t* crs_twin_pos, const double* x,
+                 double* y) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_pattern(c));
+  const size_t n = c->nr, k = c->k, nz = c->nnz_crs;
+  // twin tables to slot-major int32 (J is a slot, ell_twin_crs a CRS position)
+  std::vector<int> js(n * k), tc(n * k), cr(nz), cp(nz);
+  std::vector<uint8_t> ce(nz);
+  for (size_t i = 0; i < n; ++i)
+    for (size_t s = 0; s < k; ++s) {
+      js[s * n + i] = int(J[i * k + s]);
+      tc[s * n + i] = ell_twin_crs ? int(ell_twin_crs[i * k + s]) : -1;
+    }
+  for (size_t q = 0; q < nz; ++q) {
+    ce[q] = crs_twin_in_ell[q];
+    cr[q] = int(crs_twin_row[q]);
+    cp[q] = int(crs_twin_pos[q]);
+  }
+  DevMatrix M;
+  FVB_TRY(upload_matrix(c, M, V, crs));
+  Tmp t1, t2, t3, t4, t5, tx, ty;
+  int *dj, *dtc, *dcr, *dcp;
+  uint8_t* dce;
+  double *dx, *dy;
+  FVB_TRY(tmp_upload(c, t1, js.data(), js.size(), &dj));
+  FVB_TRY(tmp_upload(c, t2, tc.data(), tc.size(), &dtc));
+  FVB_TRY(tmp_upload(c, t3, ce.data(), ce.size(), &dce));
+  FVB_TRY(tmp_upload(c, t4, cr.data(), cr.size(), &dcr));
+  FVB_TRY(tmp_upload(c, t5, cp.data(), cp.size(), &dcp));
+  FVB_TRY(tmp_upload(c, tx, x, size_t(c->nc), &dx));
+  FVB_TRY(tmp_zero(c, ty, n, &dy));
+  FVB_TRY(stmvp(c, M.m, dj, dtc, dce, dcr, dcp, dx, dy));
+  FVB_TRY(d2h(c, y, dy, n));
   return sync(c);
 }
 

@@ -162,6 +162,11 @@ struct Ctx {
   cudaEvent_t ev[8];
   cudaEvent_t tev[2];
   cudaEvent_t kev[2];
+  // per-operator timing of one step (RunState.ops): event pairs + op ids
+  static constexpr int kOpEvents = 96;
+  cudaEvent_t opev[kOpEvents];
+  int op_id[kOpEvents / 2];
+  int n_op = 0;
   int64_t bytes = 0;
   bool have_mesh = false, have_pattern = false;
   bool have_bc[2] = {false, false};
@@ -455,6 +460,8 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
 // (implemented in fvb_ops.cu / fvb_solvers.cu / fvb_team.cu)
 int launch_inv_diag(Ctx* c, const double* V, double* inv, int* first_zero);
 int smvp(Ctx* c, MatView A, const double* x, double* y);
+int stmvp(Ctx* c, MatView A, const int* J, const int* twin_crs, const uint8_t* ct_in_ell,
+          const int* ct_row, const int* ct_pos, const double* x, double* y);
 
 struct SolveOut {
   int iterations, converged, error_kind, error_iteration;

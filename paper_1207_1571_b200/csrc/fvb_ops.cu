@@ -422,6 +422,53 @@ __global__ void k_smvp(PatternView P, const double* __restrict__ V, const double
   }
 }
 
+// stmvp (sparse.py:308-334): y = A^T x scanning row i, the value of the
+// transposed twin (c, i) of every stored (i, c) gathered through J (ELL
+// twin slot, slot-major V) or ell_twin_crs; padding contributes 0.  Same
+// einsum order as the SpMV; the CRS tail accumulates sequentially.
+template <int KT>
+__global__ void k_stmvp(PatternView P, const double* __restrict__ V, const double* __restrict__ crs,
+                        const int* __restrict__ J, const int* __restrict__ twin_crs,
+                        const uint8_t* __restrict__ ct_in_ell, const int* __restrict__ ct_row,
+                        const int* __restrict__ ct_pos, const double* __restrict__ x,
+                        double* __restrict__ y) {
+  const int n = P.n;
+  const int K = KT > 0 ? KT : P.k;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    auto term = [&](int s) {
+      const int c = P.I[size_t(s) * n + i];
+      const int col = c < 0 ? 0 : c;
+      const int js = J[size_t(s) * n + i];
+      double tv = V[size_t(js < 0 ? 0 : js) * n + col];
+      if (P.nnz_crs && js < 0) {
+        const int q = twin_crs[size_t(s) * n + i];
+        tv = crs[q < 0 ? 0 : q];
+      }
+      if (c < 0) tv = 0.0;
+      return tv * x[col];
+    };
+    double ev = term(0);
+    for (int s = 2; s < K; s += 2) ev = ev + term(s);
+    double yy = ev;
+    if (K > 1) {
+      double od = term(1);
+      for (int s = 3; s < K; s += 2) od = od + term(s);
+      yy = ev + od;
+    }
+    if (P.nnz_crs) {
+      double t = 0.0;
+      for (int q = P.crs_ptr[i]; q < P.crs_ptr[i + 1]; ++q) {
+        const int pos = ct_pos[q];
+        const double tv = ct_in_ell[q] ? V[size_t(pos < P.k - 1 ? pos : P.k - 1) * n + ct_row[q]]
+                                       : crs[pos < P.nnz_crs - 1 ? pos : P.nnz_crs - 1];
+        t += tv * x[P.crs_col[q]];
+      }
+      yy = yy + t;
+    }
+    y[i] = yy;
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------ launchers
@@ -549,6 +596,18 @@ int smvp(Ctx* c, MatView A, const double* x, double* y) {
     case 5: { k_smvp<5><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
     case 7: { k_smvp<7><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
     default: { k_smvp<0><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, x, y); fvb::note_launch(); } break;
+  }
+  FVB_CUDA(cudaGetLastError());
+  return FVB_OK;
+}
+
+int stmvp(Ctx* c, MatView A, const int* J, const int* twin_crs, const uint8_t* ct_in_ell,
+          const int* ct_row, const int* ct_pos, const double* x, double* y) {
+  PatternView P = c->pattern();
+  const int g = grid_for(c->nr, kThreads);
+  switch (c->k) {
+    case 7: { k_stmvp<7><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, J, twin_crs, ct_in_ell, ct_row, ct_pos, x, y); fvb::note_launch(); } break;
+    default: { k_stmvp<0><<<g, kThreads, 0, c->stream>>>(P, A.V, A.crs, J, twin_crs, ct_in_ell, ct_row, ct_pos, x, y); fvb::note_launch(); } break;
   }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;

@@ -330,3 +330,40 @@ extern "C" int fvb_pattern_plan_fill(fvb_pattern_plan* P, int64_t nfp,
 }
 
 extern "C" void fvb_pattern_plan_destroy(fvb_pattern_plan* P) { delete P; }
+
+// pack_q / unpack_q (sparse.py:337-363): fuse I and J into one integer
+// array Q = base*I + J (base N for mode 0 "by_N", K for mode 1 "by_K");
+// padding packs to -1, entries whose twin sits in the CRS block to -2 - I.
+extern "C" int fvb_pack_q(int64_t n, int64_t k, const int64_t* I, const int64_t* J, int mode,
+                          int64_t* q) {
+  if (mode != 0 && mode != 1) {
+    fvb_set_error("unknown mode %d", mode);
+    return FVB_E_SPARSE;
+  }
+  const int64_t base = mode == 0 ? n : k;
+  for (int64_t e = 0; e < n * k; ++e) {
+    const int64_t i = I[e], j = J[e];
+    q[e] = i < 0 ? -1 : (j < 0 ? -2 - i : base * i + j);
+  }
+  return FVB_OK;
+}
+
+extern "C" int fvb_unpack_q(int64_t n, int64_t k, int64_t m, const int64_t* q, int mode,
+                            int64_t* I, int64_t* J) {
+  if (mode != 0 && mode != 1) {
+    fvb_set_error("unknown mode %d", mode);
+    return FVB_E_SPARSE;
+  }
+  const int64_t base = mode == 0 ? n : k;
+  for (int64_t e = 0; e < m; ++e) {
+    const int64_t v = q[e];
+    if (v >= 0) {
+      I[e] = v / base;
+      J[e] = v % base;
+    } else {
+      I[e] = v == -1 ? -1 : -2 - v;
+      J[e] = -1;
+    }
+  }
+  return FVB_OK;
+}

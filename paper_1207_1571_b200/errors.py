@@ -2,7 +2,8 @@
 
 mesh.MeshError (mesh.py:27), sparse.SparseError (sparse.py:25),
 linsolve.SolverError (linsolve.py:24), fvm.FvmError (fvm.py:30),
-coupling.CouplingError (coupling.py:64), config.ConfigError (config.py:19).
+coupling.CouplingError (coupling.py:64), config.ConfigError (config.py:19),
+fileio.MeshFileError (fileio.py:27), report.ProfileError (report.py:23).
 """
 
 
@@ -27,6 +28,14 @@ class CouplingError(Exception):
 
 
 class ConfigError(Exception):
+    pass
+
+
+class MeshFileError(Exception):
+    """Malformed mesh file; message carries the line number."""
+
+
+class ProfileError(Exception):
     pass
 
 

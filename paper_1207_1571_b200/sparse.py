@@ -25,6 +25,7 @@ from .errors import SparseError
 __all__ = [
     "SparseError", "SparsityPattern", "pattern_from_pairs", "build_pattern",
     "build_pattern_from_example", "HybridMatrix", "coeff_accumulate", "diagonal", "smvp",
+    "stmvp", "pack_q", "unpack_q", "format_debug",
 ]
 
 
@@ -227,3 +228,77 @@ def smvp(A, x):
     P = _lib.ptr
     _lib.check(_lib.lib.fvb_op_smvp(ctx.h, P(V), P(crs), P(xx), P(y)))
     return y
+
+
+def stmvp(A, x):
+    """y = A^T x without forming the transpose (fvb_op_stmvp; reference
+    sparse.py:308-334): scanning row i, the value of the twin (c, i) of every
+    stored (i, c) is gathered through J or the CRS back-references — the
+    paper's column-access path (§3.1).  Same summation order as the
+    reference (einsum over the slots, then the CRS tail)."""
+    p = A.pattern
+    if len(x) != p.n:
+        raise SparseError(f"dimension mismatch: {len(x)} != {p.n}")
+    ctx = _ctx(A)
+    P = _lib.ptr
+    V = _lib.f64(A.V)
+    crs = _lib.f64(A.crs_val) if p.nnz_crs else np.zeros(1)
+    J = _lib.i64(p.J)
+    tw = _lib.i64(p.ell_twin_crs)
+    ce = np.ascontiguousarray(p.crs_twin_in_ell, dtype=np.uint8)
+    cr = _lib.i64(p.crs_twin_row)
+    cp = _lib.i64(p.crs_twin_pos)
+    xx = _lib.f64(x)
+    y = np.empty(p.n)
+    _lib.check(_lib.lib.fvb_op_stmvp(ctx.h, P(V), P(crs), P(J, _lib.i64p), P(tw, _lib.i64p),
+                                     P(ce, _lib.u8p), P(cr, _lib.i64p), P(cp, _lib.i64p),
+                                     P(xx), P(y)))
+    return y
+
+
+_Q_MODES = {"by_N": 0, "by_K": 1}
+
+
+def pack_q(pattern, mode="by_N"):
+    """Fuse I and J into one integer array Q (reference sparse.py:337-351):
+    by_N: Q = N*I + J, by_K: Q = K*I + J; padding -> -1, twin in CRS -> -2 - I."""
+    if mode not in _Q_MODES:
+        raise SparseError(f"unknown mode {mode!r}")
+    p = pattern
+    I = _lib.i64(p.I)
+    J = _lib.i64(p.J)
+    q = np.empty(I.shape, dtype=np.int64)
+    P = _lib.ptr
+    _lib.check(_lib.lib.fvb_pack_q(p.n, p.k, P(I, _lib.i64p), P(J, _lib.i64p), _Q_MODES[mode],
+                                   P(q, _lib.i64p)), SparseError)
+    return q
+
+
+def unpack_q(q, n, k, mode="by_N"):
+    """Inverse of pack_q: (I, J) exactly, sentinels included (sparse.py:354-363)."""
+    if mode not in _Q_MODES:
+        raise SparseError(f"unknown mode {mode!r}")
+    q = _lib.i64(q)
+    I = np.empty(q.shape, dtype=np.int64)
+    J = np.empty(q.shape, dtype=np.int64)
+    P = _lib.ptr
+    _lib.check(_lib.lib.fvb_unpack_q(n, k, q.size, P(q, _lib.i64p), _Q_MODES[mode],
+                                     P(I, _lib.i64p), P(J, _lib.i64p)), SparseError)
+    return I, J
+
+
+def format_debug(A):
+    """Human-readable dump of a small matrix (reference sparse.py:366-383)."""
+    p = A.pattern
+    if p.n > 16:
+        raise SparseError("debug dump limited to n <= 16")
+    lines = [f"hybrid {p.n}x{p.n}, K={p.k}, crs entries: {p.nnz_crs}"]
+    for row in A.to_dense():
+        lines.append("  [" + " ".join(f"{v:10.4g}" for v in row) + "]")
+    lines.append(f"I = {p.I.tolist()}")
+    lines.append(f"J = {p.J.tolist()}")
+    lines.append(f"V = {np.round(A.V, 6).tolist()}")
+    if p.nnz_crs:
+        lines.append(f"CRS rows {p.crs_row.tolist()} cols {p.crs_col.tolist()} "
+                     f"vals {np.round(A.crs_val, 6).tolist()}")
+    return "\n".join(lines)

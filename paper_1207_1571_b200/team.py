@@ -28,7 +28,7 @@ import threading
 import numpy as np
 
 from . import _lib
-from .coupling import _FIELD_NAMES, _step_cfg
+from .coupling import _FIELD_NAMES, _OP_NAMES, _step_cfg
 from .decompose import _Topology, build_subdomain, local_geometry, slab_partition
 from .device import DeviceContext, bc_table, device_index
 from .errors import CouplingError
@@ -152,6 +152,7 @@ class _TeamRunBase:
         self.cum_iters = {"cg": 0, "bicgstab": 0}
         self.residual_log = []
         self.wall = {}
+        self.ops = {}
         self._res_scale = {}
         self.last_solves = []
 
@@ -175,6 +176,11 @@ class _TeamRunBase:
         for key in ("momentum_assembly", "momentum_solve", "pressure_assembly",
                     "pressure_solve", "correction"):
             self.wall[key] = self.wall.get(key, 0.0) + float(getattr(rep, "t_" + key))
+        for i, name in enumerate(_OP_NAMES):
+            if rep.op_calls[i]:
+                rec = self.ops.setdefault(name, [0.0, 0])
+                rec[0] += float(rep.op_seconds[i])
+                rec[1] += int(rep.op_calls[i])
 
     def normalized(self, slot, res):
         seen = max(self._res_scale.get(slot, 0.0), res)

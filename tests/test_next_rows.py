@@ -1,0 +1,127 @@
+"""SURVEY.md §8(f) "next" rows on CPU, against golden outputs of the REAL
+reference (oracle/make_golden_next.py): native mesh-file I/O
+(fileio.py:50-185), pack_q / unpack_q (sparse.py:337-363) and the profile
+report tables (report.py:33-162)."""
+
+import json
+import os
+import types
+
+import numpy as np
+import pytest
+
+from golden_io import GOLDEN, golden_case, load
+from paper_1207_1571_b200 import cases, fileio, report, sparse
+from paper_1207_1571_b200.errors import MeshError, MeshFileError
+
+NEXT = json.load(open(os.path.join(GOLDEN, "next.json")))
+NZ = np.load(os.path.join(GOLDEN, "next.npz"))
+
+MESHES = {"cav3": lambda: cases.gen_cavity(3).mesh,
+          "chan": lambda: cases.gen_channel(6, 3).mesh,
+          "duct": lambda: cases.gen_skewed_duct(4, 3, 30.0).mesh}
+
+
+@pytest.mark.parametrize("name", sorted(MESHES))
+def test_write_mesh_is_byte_identical_to_reference(name, tmp_path):
+    p = tmp_path / f"{name}.msh"
+    fileio.write_mesh(MESHES[name](), p)
+    assert p.read_text() == NEXT["mesh_text"][name]
+
+
+@pytest.mark.parametrize("name", sorted(MESHES))
+def test_read_mesh_round_trip_exact(name, tmp_path):
+    m = MESHES[name]()
+    p = tmp_path / "m.msh"
+    p.write_text(NEXT["mesh_text"][name])
+    r = fileio.read_mesh(p)
+    for k in ("points", "face_points", "face_offsets", "owner", "neighbour"):
+        assert np.array_equal(getattr(r, k), getattr(m, k)), k
+    assert [(q.name, q.kind, q.start, q.count) for q in r.patches] == \
+        [(q.name, q.kind, q.start, q.count) for q in m.patches]
+    assert r.n_cells == m.n_cells
+    p2 = tmp_path / "again.msh"
+    fileio.write_mesh(r, p2)
+    assert p2.read_text() == NEXT["mesh_text"][name]
+
+
+@pytest.mark.parametrize("case", sorted(NEXT["bad_files"]))
+def test_read_mesh_errors_match_reference(case, tmp_path):
+    p = tmp_path / f"{case}.msh"
+    p.write_text(NEXT["bad_files"][case])
+    want = NEXT["bad_errors"][case]
+    if want[0] == "ok":
+        m = fileio.read_mesh(p)
+        assert (m.n_cells, m.n_faces) == (want[1], want[2])
+        return
+    cls = {"MeshFileError": MeshFileError, "MeshError": MeshError}[want[0]]
+    with pytest.raises(cls) as ei:
+        fileio.read_mesh(p)
+    assert str(ei.value) == want[1]
+
+
+def test_read_mesh_missing_file(tmp_path):
+    with pytest.raises(OSError):
+        fileio.read_mesh(tmp_path / "nope.msh")
+
+
+@pytest.mark.parametrize("name", ["cav6", "pcav5", "bfs2", "duct"])
+def test_pack_q_matches_reference(name):
+    case, g = golden_case(name)
+    pat = sparse.build_pattern(case.mesh)
+    for mode in ("by_N", "by_K"):
+        q = sparse.pack_q(pat, mode)
+        assert np.array_equal(q, NZ[f"{name}_q_{mode}"])
+        I, J = sparse.unpack_q(q, pat.n, pat.k, mode)
+        assert np.array_equal(I, pat.I) and np.array_equal(J, pat.J)
+
+
+@pytest.mark.parametrize("t", range(6))
+def test_pack_q_with_crs_spill(t):
+    n = int(NZ[f"rnd{t}_n"])
+    pat = sparse.pattern_from_pairs(n, NZ[f"rnd{t}_pairs"], int(NZ[f"rnd{t}_kcap"]))
+    assert pat.nnz_crs == int(NZ[f"rnd{t}_nnz_crs"])
+    for mode in ("by_N", "by_K"):
+        q = sparse.pack_q(pat, mode)
+        assert np.array_equal(q, NZ[f"rnd{t}_q_{mode}"])
+        I, J = sparse.unpack_q(q, n, pat.k, mode)
+        assert np.array_equal(I, pat.I) and np.array_equal(J, pat.J)
+    with pytest.raises(sparse.SparseError):
+        sparse.pack_q(pat, "by_X")
+
+
+def _synthetic_state():
+    p = NEXT["profile"]
+    st = types.SimpleNamespace(
+        wall=dict(p["sections"]),
+        residual_log=[("bicgstab", "ux", 1, 12, 1.0, 1e-9), ("bicgstab", "uy", 1, 11, 1.0, 1e-9),
+                      ("bicgstab", "uz", 1, 0, 0.0, 0.0), ("cg", "p", 1, 140, 1.0, 1e-11),
+                      ("cg", "p", 1, 133, 0.3, 1e-11)],
+        stage_times={k: dict(v["stages"]) for k, v in p["solvers"].items()},
+        ops={k: [v["seconds"], v["calls"]] for k, v in p["ops"].items()},
+        cum_iters=dict(p["cum_iters"]), outer=p["outer"], converged=p["converged"])
+    return st
+
+
+def test_profile_and_tables_match_reference():
+    prof = report.collect_profile(_synthetic_state())
+    assert json.loads(json.dumps(prof)) == NEXT["profile"]
+    for name, fn in (("solver_share", report.solver_share_table),
+                     ("cg_stage", report.cg_stage_table),
+                     ("assembly_norm", report.assembly_norm_table)):
+        h, rows = fn(prof)
+        assert json.loads(json.dumps([h, rows])) == NEXT["tables"][name]
+    assert report.format_tables(prof) == NEXT["format_tables"]
+
+
+def test_profile_errors():
+    st = _synthetic_state()
+    del st.wall["total"]
+    with pytest.raises(report.ProfileError, match="no recorded wall time"):
+        report.collect_profile(st)
+    st = _synthetic_state()
+    st.stage_times = {}
+    prof = report.collect_profile(st)
+    with pytest.raises(report.ProfileError, match="no stage data recorded for cg"):
+        report.cg_stage_table(prof)
+    assert "stage tables unavailable" in report.format_tables(prof)
