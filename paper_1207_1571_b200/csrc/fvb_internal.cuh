@@ -379,6 +379,39 @@ __device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
   return true;
 }
 
+// Scoped atomics / loads of the grid barrier.  Arrival is an acq_rel
+// atomic (release orders this block's partials and stores; the returned
+// count tells the last arriver, whose acquire makes every partial visible);
+// the release of the generation word orders the broadcast; waiters poll
+// relaxed and finish with one acquire load (which also invalidates this
+// SM's L1, so stale lines of the previous pass are never read).  Scope is
+// the GPU, or the system when the mesh is decomposed over several devices
+// (halo stores to peers must be ordered before the peers' mailbox flags).
+__device__ __forceinline__ unsigned atom_arrive(unsigned* p, bool sys) {
+  unsigned o;
+  if (sys)
+    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(o) : "l"(p) : "memory");
+  else
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(o) : "l"(p) : "memory");
+  return o;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, bool sys) {
+  if (sys)
+    asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+  else
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // Grid(+team)-wide deterministic sum of M doubles for co-resident
 // (cooperatively launched) grids.  v holds each thread's partial sums on
 // entry and the global sums on exit, bit-identical in every thread of every
@@ -394,22 +427,20 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* smem /*[32*M+M]*/) {
   __shared__ int s_last, s_ok;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool sys = T.size > 1;
   block_reduce<M>(v, smem);
-  volatile unsigned* vgen = sync + 1;
   volatile unsigned* vabort = sync + 2;
   double* bcast = reinterpret_cast<double*>(sync + 4);
   unsigned gen = 0;
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int m = 0; m < M; ++m) partials[size_t(m) * gridDim.x + blockIdx.x] = v[m];
-    gen = *vgen;
-    if (T.size > 1) __threadfence_system(); else __threadfence();
-    s_last = atomicAdd(sync, 1u) == gridDim.x - 1;
+    gen = ld_relaxed_gpu(sync + 1);
+    s_last = atom_arrive(sync, sys) == gridDim.x - 1;
   }
   __syncthreads();
   if (s_last) {
     if (warp == 0) {
-      __threadfence();
       double r[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
@@ -426,24 +457,24 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
         if (!ok) *vabort = 1u;
 #pragma unroll
         for (int m = 0; m < M; ++m) __stcg(bcast + m, r[m]);
-        atomicExch(sync, 0u);
-        __threadfence();
-        atomicAdd(sync + 1, 1u);
+        sync[0] = 0u;  // reset arrivals; ordered before the release below
+        red_release_add(sync + 1, sys);
       }
     }
   } else if (threadIdx.x == 0) {
     const uint64_t t0 = global_ns();
-    while (*vgen == gen) {
+    int spins = 0;
+    while (ld_relaxed_gpu(sync + 1) == gen) {
       if (*vabort) break;
-      __nanosleep(20);
-      if (global_ns() - t0 > kWatchdogNs + 2000000000ull) {
+      if (++spins > 64) __nanosleep(32);
+      if ((spins & 1023) == 0 && global_ns() - t0 > kWatchdogNs + 2000000000ull) {
         atomicExch(sync + 2, 1u);
         break;
       }
     }
   }
   if (threadIdx.x == 0) {
-    __threadfence();  // gpu-scope fence: also invalidates this SM's L1
+    ld_acquire_gpu(sync + 1);  // acquire (+ L1 invalidate) before reading results
     s_ok = *vabort == 0;
 #pragma unroll
     for (int m = 0; m < M; ++m) smem[32 * M + m] = __ldcg(bcast + m);

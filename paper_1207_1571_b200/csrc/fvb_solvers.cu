@@ -64,12 +64,26 @@ __device__ __forceinline__ T ld_mat(const T* p) {
 // Variant of the pipelined pass A that prefetches only the column indices
 // (the gather's address chain) DEPTH rows ahead; the values V of the current
 // row are loaded in-iteration (they are off the critical path).
-template <int KT, int DEPTH, bool HINT>
+// load the index ring of the first DEPTH rows of a sweep
+template <int KT, int DEPTH>
+__device__ __forceinline__ void icols_ring_load(const PatternView& P, int (&cq)[DEPTH][KT], int i,
+                                                int end, int step) {
+#pragma unroll
+  for (int d = 0; d < DEPTH; ++d) {
+    const int r = i + d * step;
+    if (r < end) {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) cq[d][s] = __ldcs(P.I + size_t(s) * P.n + r);
+    }
+  }
+}
+
+template <int KT, int DEPTH, bool PRE>
 __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const double* __restrict__ z,
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
                                                   bool first, int slot_new, int i, int end,
-                                                  int step) {
+                                                  int step, int (&cq)[DEPTH][KT]) {
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int n = P.n;
@@ -77,15 +91,9 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
   const double* __restrict__ V = A.V;
   const bool team = T.size > 1;
   double acc = 0.0;
-  int cq[DEPTH][KT];
-#pragma unroll
-  for (int d = 0; d < DEPTH; ++d) {
-    const int r = i + d * step;
-    if (r < end) {
-#pragma unroll
-      for (int s = 0; s < KT; ++s) cq[d][s] = __ldcs(I + size_t(s) * n + r);
-    }
-  }
+  // PRE: the caller loaded the ring before the barrier that precedes this
+  // pass, so the first rows' address chain is already resolved
+  if (!PRE) icols_ring_load<KT, DEPTH>(P, cq, i, end, step);
   auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
   while (i < end) {
     double vi[KT];
@@ -124,7 +132,6 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
     acc += pi * qi;
     i += step;
   }
-  (void)HINT;
   return acc;
 }
 
@@ -195,7 +202,7 @@ __device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double
 // gives every block one contiguous chunk swept in blockDim steps, so the
 // +-1 and +-n neighbours a row gathers were loaded by the same SM moments
 // earlier (L1 hits) and only the +-n^2 ones come from L2.
-template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0>
+template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
   const PatternView& P = A.P;
@@ -252,6 +259,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   bool first = true;
   uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
   const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+  constexpr int KR = KT > 0 ? KT : 1;
+  constexpr int DR = PIPE >= 4 ? PIPE - 2 : 1;
+  int ring[DR][KR];
+  if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
   while (!conv && it < A.max_iters) {
     ++it;
     if (timer) tk = global_ns();
@@ -261,8 +272,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
       if (PIPE >= 3 && KT > 0) {
-        pq[0] = cg_pass_a_icols<(KT > 0 ? KT : 1), (PIPE >= 4 ? PIPE - 2 : 1), false>(
-            A, z, po, pnew, beta, first, slot_new, tid, n, G);
+        pq[0] = cg_pass_a_icols<KR, DR, (XB != 0)>(A, z, po, pnew, beta, first, slot_new, tid,
+                                                   n, G, ring);
       } else if (PIPE && KT > 0) {
         pq[0] = cg_pass_a_pipe<(KT > 0 ? KT : 1), (PIPE > 1)>(A, z, po, pnew, beta, first,
                                                                 slot_new, tid, n, G);
@@ -296,6 +307,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s2[0] += ri * ri;
       s2[1] += ri * zi;
     }
+    // next pass A's first index rows travel while this pass's reduction runs
+    if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
     if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
     if (!team_reduce<2>(T, A.sync, A.partials, s2, red)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
@@ -456,8 +469,8 @@ struct CompState {
   double bn, res0, res, rho, alpha, omega, beta, rr, rhr;
 };
 
-template <int KT, int NC>
-__global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab(BiParams<NC> A) {
+template <int KT, int NC, int THREADS = kSolverThreads, int MINB = 2>
+__global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
   __shared__ double red[32 * 2 * NC + 2 * NC];
   __shared__ CompState S[NC];
   const PatternView& P = A.P;
@@ -852,14 +865,14 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   // FVB_CG_VARIANT selects an alternative kernel configuration (tuning
   // experiments, tools/cg_micro.py); the default is the measured best:
   // pass A with the column indices prefetched two rows ahead (the gather's
-  // address chain), evict-first matrix loads, grid-strided rows, 2 x 512
-  // threads per SM (profiles/r01_cg_variants.md).
+  // address chain), evict-first matrix loads, grid-strided rows, one
+  // 1024-thread block per SM (profiles/r01_cg_variants.md).
   static const int variant = [] {
     const char* e = getenv("FVB_CG_VARIANT");
     return e ? atoi(e) : -1;
   }();
   switch (c->k) {
-    case 5: FVB_TRY(coop_launch(c, k_cg<5, 512, 2, 4>, prm)); break;
+    case 5: FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4>, prm, 1024, 1)); break;
     case 7:
       switch (variant) {
         case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;
@@ -878,8 +891,10 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
         case 14: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 5>, prm)); break;
         case 15: FVB_TRY(coop_launch(c, k_cg<7, 256, 4, 4>, prm, 256, 4)); break;
         case 16: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 6>, prm)); break;
+        case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;
+        case 19: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 1>, prm, 1024, 1)); break;
         case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;
-        default: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;
+        default: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;
       }
       break;
     default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
@@ -936,9 +951,15 @@ static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const*
   prm.sync = c->sync;
   prm.partials = c->partials;
   prm.result = result;
+  static const int variant = [] {
+    const char* e = getenv("FVB_BI_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
   switch (c->k) {
     case 5: return coop_launch(c, k_bicgstab<5, NC>, prm);
-    case 7: return coop_launch(c, k_bicgstab<7, NC>, prm);
+    case 7:
+      if (variant == 1) return coop_launch(c, k_bicgstab<7, NC, 1024, 1>, prm, 1024, 1);
+      return coop_launch(c, k_bicgstab<7, NC>, prm);
     default: return coop_launch(c, k_bicgstab<0, NC>, prm);
   }
 }

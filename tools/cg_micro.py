@@ -27,10 +27,12 @@ for rpt in range(3):
     rc = _lib.lib.fvb_op_cg(ctx.h, P(_lib.f64(V)), P(crs), P(b), P(np.zeros(N)), P(x), 1e-300, 0.0,
                             iters, C.byref(rep))
     _lib.check(rc)
-    res.append(rep.wall_time)
-t = min(res)
+    res.append((rep.wall_time, rep.t_smvp, rep.t_daxpy, rep.t_reduction))
+t, ta, tb, tr = min(res)
 bytes_it = N * (12 * K + 96)
 setup_b = N * (12 * K + 80)
 print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "0"), "n": n, "iters": rep.iterations,
                   "us_per_iter": 1e6 * t / iters,
+                  "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
+                  "us_reduce2x": 1e6 * tr / iters,
                   "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1)}))
