@@ -753,6 +753,321 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
   }
 }
 
+// ------------------------------------------------------ BiCGStab, 3 passes
+// The same algorithm and rounding as k_bicgstab (linsolve.py:175-282) with
+// the vector passes fused away: p_hat and s_hat are never
+// stored — every SpMV rebuilds them for the gathered columns from r, p, v
+// and 1/D exactly as the 5-pass kernel computes them, and the update pass
+// rebuilds them for the own row.  Three reductions per iteration: r_hat.v;
+// ||s||^2, t.t, t.s (t is formed speculatively and dropped when s already
+// converged); ||r||^2, r_hat.r.  p and v are double-buffered because pass 1
+// gathers the previous ones while writing the new ones.  Decomposed runs
+// send the new p and v (pass 1) and r (pass 3) of processor-boundary rows,
+// and 1/D and r once at setup.
+template <int NC>
+struct Bi3Params {
+  PatternView P;
+  TeamView T;
+  const double* V;
+  const double* crs;
+  double* inv;
+  const double* b[NC];
+  double* x[NC];
+  double* r[NC];
+  double* rh[NC];
+  double* p[2][NC];
+  double* v[2][NC];
+  double* t[NC];
+  int slot_inv, slot_r[NC], slot_p[2][NC], slot_v[2][NC];
+  double tol, abs_tol;
+  int max_iters;
+  unsigned* sync;
+  double* partials;
+  double* result;
+};
+
+template <int KT, int NC>
+__global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A) {
+  __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
+  __shared__ CompState S[NC];
+  const PatternView& P = A.P;
+  const TeamView& T = A.T;
+  const int n = P.n;
+  const int G = gridDim.x * blockDim.x;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool team = T.size > 1;
+  const double* __restrict__ inv = A.inv;
+  bool act[NC];
+  bool timeout = false;
+  constexpr int KR = KT > 0 ? KT : 1;
+
+  // setup (linsolve.py:180-196): r = b - A x0, r_hat = r, ||b||, ||r||
+  double sums[2 * NC];
+  {
+#pragma unroll
+    for (int m = 0; m < 2 * NC; ++m) sums[m] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) act[c] = true;
+    for (int i = tid; i < n; i += G) {
+      double ax[NC];
+      auto g = [&](int c, int col) { return A.x[c][col]; };
+      ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, ax);
+      const bool snd = team && i >= T.n_inner;
+      if (snd) halo_send(T, i, A.slot_inv, inv[i]);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const double bi = A.b[c][i];
+        const double ri = bi - ax[c];
+        A.r[c][i] = ri;
+        A.rh[c][i] = ri;
+        if (snd) halo_send(T, i, A.slot_r[c], ri);
+        sums[2 * c] += bi * bi;
+        sums[2 * c + 1] += ri * ri;
+      }
+    }
+  }
+  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red)) {
+    if (tid == 0)
+      for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < NC; ++c) {
+      CompState& q = S[c];
+      q.it = 0; q.err = SE_NONE; q.err_it = 0; q.sconv = 0; q.restart = 0; q.copy = 0; q.live = 0;
+      q.bn = fmax(sqrt(sums[2 * c]), kResFloor);
+      q.res = sqrt(sums[2 * c + 1]) / q.bn;
+      q.res0 = q.res;
+      q.rr = sums[2 * c + 1];
+      q.rhr = q.rr;
+      q.done = q.res <= A.tol || q.res * q.bn <= A.abs_tol;
+      q.rho = q.alpha = q.omega = 1.0;
+      q.beta = 0.0;
+    }
+  }
+  __syncthreads();
+
+  uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
+  const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
+  int cur = 0;  // p[cur], v[cur]: previous iteration; p[nxt], v[nxt]: this one
+  while (!timeout) {
+    if (timer) tk = global_ns();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < NC; ++c) {
+        CompState& q = S[c];
+        q.sconv = 0;
+        q.live = 0;
+        if (q.done || q.err || q.it >= A.max_iters) continue;
+        q.it++;
+        double rho_new = q.it == 1 ? q.rr : q.rhr;
+        q.restart = fabs(rho_new) < kTiny;
+        if (q.restart) {
+          rho_new = q.rr;  // r_hat := r, so r_hat.r = ||r||^2
+          if (rho_new < kTiny) { q.err = SE_RHO; q.err_it = q.it; continue; }
+        }
+        q.copy = (q.it == 1 || q.restart);
+        if (!q.copy) q.beta = (rho_new / q.rho) * (q.alpha / q.omega);
+        q.rho = rho_new;
+        q.live = 1;
+      }
+    }
+    __syncthreads();
+    bool any = false;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      act[c] = S[c].live != 0;
+      any = any || act[c];
+    }
+    if (!any) break;
+    const int nxt = cur ^ 1;
+    // pass 1: p = r | r + beta (p - omega v); v = A (p / D) rebuilt per
+    // gathered column; r_hat.v
+    {
+      double rv[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) rv[c] = 0.0;
+      bool cp[NC];
+      double be[NC], om[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        cp[c] = S[c].copy != 0;
+        be[c] = S[c].beta;
+        om[c] = S[c].omega;
+      }
+      auto pval = [&](int c, int col) {
+        const double ri = A.r[c][col];
+        if (cp[c]) return ri;
+        double pi = A.p[cur][c][col] - om[c] * A.v[cur][c][col];
+        pi = pi * be[c];
+        return pi + ri;
+      };
+      auto g = [&](int c, int col) { return pval(c, col) * inv[col]; };
+      auto body = [&](int i, const double* y) {
+        const bool snd = team && i >= T.n_inner;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          const double pi = pval(c, i);
+          A.p[nxt][c][i] = pi;
+          A.v[nxt][c][i] = y[c];
+          double rhi;
+          if (S[c].restart) {
+            rhi = A.r[c][i];
+            A.rh[c][i] = rhi;
+          } else {
+            rhi = A.rh[c][i];
+          }
+          if (snd) {
+            halo_send(T, i, A.slot_p[nxt][c], pi);
+            halo_send(T, i, A.slot_v[nxt][c], y[c]);
+          }
+          rv[c] += rhi * y[c];
+        }
+      };
+      if (KT > 0) {
+        spmv_sweep<KR, NC>(P, A.V, A.crs, tid, n, G, act, g, body);
+      } else {
+        for (int i = tid; i < n; i += G) {
+          double y[NC];
+          ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
+          body(i, y);
+        }
+      }
+      if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          if (fabs(rv[c]) < kTiny) { S[c].err = SE_RV; S[c].err_it = S[c].it; continue; }
+          S[c].alpha = S[c].rho / rv[c];
+        }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < NC; ++c) act[c] = act[c] && !S[c].err;
+    }
+    // pass 2: s = r - alpha v, t = A (s / D) rebuilt per gathered column;
+    // ||s||^2, t.t, t.s
+    {
+      double st[3 * NC];
+#pragma unroll
+      for (int m = 0; m < 3 * NC; ++m) st[m] = 0.0;
+      double al[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) al[c] = S[c].alpha;
+      auto sval = [&](int c, int col) { return A.r[c][col] - al[c] * A.v[nxt][c][col]; };
+      auto g = [&](int c, int col) { return sval(c, col) * inv[col]; };
+      auto body = [&](int i, const double* y) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          const double si = sval(c, i);
+          A.t[c][i] = y[c];
+          st[3 * c] += si * si;
+          st[3 * c + 1] += y[c] * y[c];
+          st[3 * c + 2] += y[c] * si;
+        }
+      };
+      bool any_a = false;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) any_a = any_a || act[c];
+      if (KT > 0 && any_a) {
+        spmv_sweep<KR, NC>(P, A.V, A.crs, tid, n, G, act, g, body);
+      } else {
+        for (int i = tid; i < n; i += G) {
+          double y[NC];
+          ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
+          body(i, y);
+        }
+      }
+      if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
+      if (!team_reduce<3 * NC>(T, A.sync, A.partials, st, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          const double sn = sqrt(st[3 * c]);
+          if (sn / S[c].bn <= A.tol || sn <= A.abs_tol) {  // linsolve.py:234-245
+            S[c].sconv = 1;
+            S[c].res = sn / S[c].bn;
+            continue;
+          }
+          const double tt = st[3 * c + 1], ts = st[3 * c + 2];
+          if (tt == 0.0) { S[c].err = SE_OMEGA; S[c].err_it = S[c].it; continue; }
+          S[c].omega = ts / tt;
+          if (fabs(S[c].omega) < kTiny) { S[c].err = SE_OMEGA; S[c].err_it = S[c].it; }
+        }
+      __syncthreads();
+    }
+    // pass 3: x += alpha p_hat (+ omega s_hat); r = s - omega t; ||r||^2, r_hat.r
+    {
+      double rr[2 * NC];
+#pragma unroll
+      for (int m = 0; m < 2 * NC; ++m) rr[m] = 0.0;
+      bool xa[NC], full[NC];
+      double al[NC], om[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        // s-converged components take x += alpha p_hat only; erred ones nothing
+        xa[c] = act[c] && (S[c].sconv || !S[c].err);
+        full[c] = act[c] && !S[c].sconv && !S[c].err;
+        al[c] = S[c].alpha;
+        om[c] = S[c].omega;
+      }
+      for (int i = tid; i < n; i += G) {
+        const double iv = inv[i];
+        const bool snd = team && i >= T.n_inner;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (!xa[c]) continue;
+          const double phi = A.p[nxt][c][i] * iv;
+          double xi = A.x[c][i] + al[c] * phi;
+          if (full[c]) {
+            const double si = A.r[c][i] - al[c] * A.v[nxt][c][i];
+            const double shi = si * iv;
+            xi = xi + om[c] * shi;
+            const double ri = si - om[c] * A.t[c][i];
+            A.r[c][i] = ri;
+            if (snd) halo_send(T, i, A.slot_r[c], ri);
+            rr[2 * c] += ri * ri;
+            rr[2 * c + 1] += A.rh[c][i] * ri;
+          }
+          A.x[c][i] = xi;
+        }
+      }
+      if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red)) { timeout = true; break; }
+      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
+      if (threadIdx.x == 0)
+        for (int c = 0; c < NC; ++c) {
+          if (!act[c]) continue;
+          if (S[c].sconv) { S[c].done = 1; continue; }
+          if (!full[c]) continue;
+          S[c].rr = rr[2 * c];
+          S[c].rhr = rr[2 * c + 1];
+          S[c].res = sqrt(rr[2 * c]) / S[c].bn;
+          if (!isfinite(S[c].res)) { S[c].err = SE_DIVERGED; S[c].err_it = S[c].it; continue; }
+          if (S[c].res <= A.tol || S[c].res * S[c].bn <= A.abs_tol) S[c].done = 1;
+        }
+      __syncthreads();
+    }
+    cur = nxt;
+  }
+  if (tid == 0) {
+    for (int c = 0; c < NC; ++c) {
+      A.result[6 * c + 0] = S[c].it;
+      A.result[6 * c + 1] = S[c].done ? 1.0 : 0.0;
+      A.result[6 * c + 2] = S[c].res0;
+      A.result[6 * c + 3] = S[c].res;
+      A.result[6 * c + 4] = timeout ? SE_TIMEOUT : S[c].err;
+      A.result[6 * c + 5] = S[c].err_it;
+    }
+    A.result[18] = 1e-9 * double(t_spmv);
+    A.result[19] = 1e-9 * double(t_axpy);
+    A.result[20] = 1e-9 * double(t_red);
+  }
+}
+
 template <typename K>
 int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   int per_sm = 0;
@@ -951,16 +1266,49 @@ static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const*
   prm.sync = c->sync;
   prm.partials = c->partials;
   prm.result = result;
-  static const int variant = [] {
-    const char* e = getenv("FVB_BI_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
   switch (c->k) {
     case 5: return coop_launch(c, k_bicgstab<5, NC>, prm);
-    case 7:
-      if (variant == 1) return coop_launch(c, k_bicgstab<7, NC, 1024, 1>, prm, 1024, 1);
-      return coop_launch(c, k_bicgstab<7, NC>, prm);
+    case 7: return coop_launch(c, k_bicgstab<7, NC>, prm);
     default: return coop_launch(c, k_bicgstab<0, NC>, prm);
+  }
+}
+
+// 3-pass kernel (default); FVB_BI_VARIANT=5 selects the 5-pass one
+template <int NC>
+static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const* x, double tol,
+                        double abs_tol, int max_iters, double* inv, double* result) {
+  Bi3Params<NC> prm;
+  prm.P = c->pattern();
+  prm.T = c->team;
+  prm.V = A.V;
+  prm.crs = A.crs;
+  prm.inv = inv;
+  prm.slot_inv = S_SCR + 0;
+  int s = S_SCR + 1;
+  for (int k = 0; k < NC; ++k) {
+    prm.b[k] = b[k];
+    prm.x[k] = x[k];
+    prm.slot_r[k] = s;
+    prm.r[k] = c->slot(s++);
+    prm.rh[k] = c->slot(s++);
+    for (int q = 0; q < 2; ++q) {
+      prm.slot_p[q][k] = s;
+      prm.p[q][k] = c->slot(s++);
+      prm.slot_v[q][k] = s;
+      prm.v[q][k] = c->slot(s++);
+    }
+    prm.t[k] = c->slot(s++);
+  }
+  prm.tol = tol;
+  prm.abs_tol = abs_tol;
+  prm.max_iters = max_iters;
+  prm.sync = c->sync;
+  prm.partials = c->partials;
+  prm.result = result;
+  switch (c->k) {
+    case 5: return coop_launch(c, k_bicgstab3<5, NC>, prm);
+    case 7: return coop_launch(c, k_bicgstab3<7, NC>, prm);
+    default: return coop_launch(c, k_bicgstab3<0, NC>, prm);
   }
 }
 
@@ -981,10 +1329,21 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
     return FVB_E_ARG;
   }
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
-  if (ncomp == 1)
-    FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
-  else
-    FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  static const bool five = [] {
+    const char* e = getenv("FVB_BI_VARIANT");
+    return e && atoi(e) == 5;
+  }();
+  if (five) {
+    if (ncomp == 1)
+      FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+    else
+      FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  } else {
+    if (ncomp == 1)
+      FVB_TRY(bicg3_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+    else
+      FVB_TRY(bicg3_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  }
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[21];
   unsigned team_err = 0;
