@@ -351,21 +351,29 @@ __device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
   const unsigned long long ep = *vep + 1;
   *vep = ep;
   const int par = int(ep & 1ull);
-  __threadfence_system();  // order this rank's halo stores before the message
+  // This rank's halo stores are already ordered before this thread (the
+  // blocks' sys-scope acq_rel arrivals, or the fence.sys that ends every
+  // halo-push thread); one fence then orders the payloads before the flags.
   for (int q = 0; q < T.size; ++q) {
     Comm* pc = T.peer_comm[q];
 #pragma unroll
     for (int m = 0; m < M; ++m) pc->mail[par][T.rank][m] = v[m];
   }
   __threadfence_system();
-  for (int q = 0; q < T.size; ++q) st_release_sys(&T.peer_comm[q]->seq[T.rank], ep);
+  for (int q = 0; q < T.size; ++q)
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&T.peer_comm[q]->seq[T.rank]),
+                 "l"(ep)
+                 : "memory");
   const uint64_t t0 = global_ns();
   for (int q = 0; q < T.size; ++q) {
-    while (ld_acquire_sys(&me->seq[q]) < ep) {
+    for (;;) {
+      unsigned long long sq;
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(sq) : "l"(&me->seq[q]) : "memory");
+      if (sq >= ep) break;
       if (global_ns() - t0 > kWatchdogNs) return false;
-      __nanosleep(32);
     }
   }
+  ld_acquire_sys(&me->seq[T.rank]);  // acquire: the mailboxes below are current
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     const volatile double* box = &me->mail[par][0][m];
@@ -426,39 +434,50 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
                                             double* smem /*[32*M+M]*/) {
   __shared__ int s_last, s_ok;
+  __shared__ unsigned s_gen;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool sys = T.size > 1;
   block_reduce<M>(v, smem);
   volatile unsigned* vabort = sync + 2;
   double* bcast = reinterpret_cast<double*>(sync + 4);
-  unsigned gen = 0;
   if (threadIdx.x == 0) {
+    const unsigned gen = ld_relaxed_gpu(sync + 1);
+    s_gen = gen;
+    // partials double-buffered by generation parity: a block can only write
+    // the partial of reduction k+2 after every block passed reduction k+1,
+    // i.e. after every block finished reading the partials of reduction k
+    double* part = partials + size_t(gen & 1u) * size_t(M) * gridDim.x;
 #pragma unroll
-    for (int m = 0; m < M; ++m) partials[size_t(m) * gridDim.x + blockIdx.x] = v[m];
-    gen = ld_relaxed_gpu(sync + 1);
+    for (int m = 0; m < M; ++m) part[size_t(m) * gridDim.x + blockIdx.x] = v[m];
     s_last = atom_arrive(sync, sys) == gridDim.x - 1;
   }
   __syncthreads();
+  const unsigned gen = s_gen;
+  const double* part = partials + size_t(gen & 1u) * size_t(M) * gridDim.x;
   if (s_last) {
-    if (warp == 0) {
+    if (!sys) {
+      if (threadIdx.x == 0) {
+        sync[0] = 0u;  // reset arrivals; ordered before the release below
+        red_release_add(sync + 1, false);
+      }
+    } else if (warp == 0) {
+      // decomposed mesh: this rank's sum goes through the peer mailboxes
       double r[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         double x = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32)
-          x += __ldcg(partials + size_t(m) * gridDim.x + b);
+        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(part + size_t(m) * gridDim.x + b);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
         r[m] = x;
       }
       if (lane == 0) {
-        bool ok = true;
-        if (T.size > 1) ok = team_exchange<M>(T, r, RED_SUM);
+        const bool ok = team_exchange<M>(T, r, RED_SUM);
         if (!ok) *vabort = 1u;
 #pragma unroll
         for (int m = 0; m < M; ++m) __stcg(bcast + m, r[m]);
-        sync[0] = 0u;  // reset arrivals; ordered before the release below
-        red_release_add(sync + 1, sys);
+        sync[0] = 0u;
+        red_release_add(sync + 1, true);
       }
     }
   } else if (threadIdx.x == 0) {
@@ -476,10 +495,26 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   if (threadIdx.x == 0) {
     ld_acquire_gpu(sync + 1);  // acquire (+ L1 invalidate) before reading results
     s_ok = *vabort == 0;
+    if (sys) {
 #pragma unroll
-    for (int m = 0; m < M; ++m) smem[32 * M + m] = __ldcg(bcast + m);
+      for (int m = 0; m < M; ++m) smem[32 * M + m] = __ldcg(bcast + m);
+    }
   }
   __syncthreads();
+  if (!sys && warp == 0) {
+    // single device: every block sums the partials itself, in the same
+    // fixed order (lane-strided over blocks, then a shuffle tree)
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double x = 0.0;
+      for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(part + size_t(m) * gridDim.x + b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      if (lane == 0) smem[32 * M + m] = x;
+    }
+    __syncwarp();
+  }
+  if (!sys) __syncthreads();
 #pragma unroll
   for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
   const bool ok = s_ok != 0;
