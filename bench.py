@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cg-sample", type=int, default=20)
+    ap.add_argument("--no-aux", action="store_true",
+                    help="skip the auxiliary C2 (128^3) measurement at N=1")
     return ap.parse_args()
 
 
@@ -332,6 +334,41 @@ class _Dist:
             self.dist.destroy_process_group()
 
 
+def measure_c2(steps, warmup):
+    """BASELINE configs[1] (gen_cavity(128), 1 B200) device-timed, for
+    reference next to the C5 headline (not the bench line's value)."""
+    import ctypes as C
+
+    from paper_1207_1571_b200 import _lib
+    from paper_1207_1571_b200.coupling import CouplingConfig, init_state, piso_time_step
+
+    case = make_case(128)
+    cfg = CouplingConfig.from_case_config(case.config)
+    st = init_state(case, cfg)
+    h = st._ctx.h
+    for _ in range(warmup):
+        piso_time_step(st, cfg)
+    rows = []
+    _lib.check(_lib.lib.fvb_sync(h))
+    _lib.check(_lib.lib.fvb_timer_start(h))
+    for _ in range(steps):
+        piso_time_step(st, cfg)
+        rows.extend(st._last_solves)
+    ms = C.c_double()
+    _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
+    N, K = case.mesh.n_cells, st.pattern.k
+    cg = [(it, ks) for sv, it, ks in rows if sv == "cg"]
+    cg_bytes = sum(N * (12 * K + 80) + it * N * (12 * K + 96) for it, _ in cg)
+    cg_time = sum(ks for _, ks in cg)
+    peak, _ = peaks()
+    ms_step = ms.value / steps
+    return {"workload": "C2 gen_cavity(128) PISO dt=0.1/128, reference defaults",
+            "cells": N, "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
+            "value": N / (ms_step / 1e3), "unit": "cell-updates/s",
+            "k_cg_gbs": cg_bytes / cg_time / 1e9, "k_cg_frac": cg_bytes / cg_time / 1e9 / peak,
+            "cg_iters_per_step": sum(it for it, _ in cg) / steps}
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -469,6 +506,10 @@ def run_ours(args):
                               f"{counts['cg']:.0f}, BiCGStab {counts['bicgstab']:.0f} per step); "
                               f"OpenBLAS default threads; {d['sample_s']:.1f} s of CPU work"),
                    "s_per_step": d["s_per_step"]}
+    # ------------------------------------------- auxiliary C2 (configs[1])
+    aux = None
+    if D.world == 1 and n != 128 and not args.no_aux:
+        aux = measure_c2(steps=3, warmup=2)
     out = {
         "metric": METRIC,
         "value": N / (ms_step / 1e3),
@@ -509,6 +550,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
         "cpu_baseline": cpu,
+        "aux_c2_128": aux,
     }
     if D.rank == 0:
         print(json.dumps(out))

@@ -373,7 +373,9 @@ __device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
       if (global_ns() - t0 > kWatchdogNs) return false;
     }
   }
-  ld_acquire_sys(&me->seq[T.rank]);  // acquire: the mailboxes below are current
+  // relaxed reads that observed every flag + fence = acquire (the
+  // mailboxes and the peers' halo stores below are current)
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     const volatile double* box = &me->mail[par][0][m];
