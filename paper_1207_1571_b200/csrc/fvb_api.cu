@@ -304,8 +304,6 @@ int ensure_work(Ctx* c) {
   return FVB_OK;
 }
 
-void drop_ext(Ctx*) {}
-
 void fill_report(fvb_solve_report& r, const SolveOut& o) {
   r.iterations = o.iterations;
   r.converged = o.converged;
@@ -641,7 +639,6 @@ int fvb_ctx_destroy(fvb_ctx* h) {
   for (auto& ev : c->opev)
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
-  drop_ext(c);
   delete h;
   return FVB_OK;
 }

@@ -1084,7 +1084,6 @@ int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
 
 template <typename K, typename Args>
 int coop_launch(Ctx* c, K kernel, Args& args, int threads = kSolverThreads, int max_per_sm = 2) {
-  const int kSolverThreads = threads;
   int blocks = 0;
   FVB_TRY(coop_blocks(c, kernel, threads, max_per_sm, &blocks));
   // words 0-2: arrivals, generation, abort; word 3 (team error) is sticky
@@ -1095,10 +1094,10 @@ int coop_launch(Ctx* c, K kernel, Args& args, int threads = kSolverThreads, int 
     // several ranks share this device: each grid is sized to 1/share of the
     // resident capacity, so the ranks' grids are co-resident together; a
     // plain launch avoids relying on concurrent cooperative launches
-    FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads), params, 0,
+    FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(blocks), dim3(threads), params, 0,
                               c->stream));
   } else {
-    FVB_CUDA(cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(kSolverThreads),
+    FVB_CUDA(cudaLaunchCooperativeKernel((const void*)kernel, dim3(blocks), dim3(threads),
                                          params, 0, c->stream));
   }
   return FVB_OK;
@@ -1190,25 +1189,10 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
     case 5: FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4>, prm, 1024, 1)); break;
     case 7:
       switch (variant) {
-        case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;
-        case 1: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 1>, prm, 512, 2)); break;
-        case 2: FVB_TRY(coop_launch(c, k_cg<7, 256, 3, 1>, prm, 256, 3)); break;
-        case 3: FVB_TRY(coop_launch(c, k_cg<7, 512, 1, 1>, prm, 512, 1)); break;
-        case 4: FVB_TRY(coop_launch(c, k_cg<7, 256, 4, 0>, prm, 256, 4)); break;
-        case 5: FVB_TRY(coop_launch(c, k_cg<7, 384, 2, 1>, prm, 384, 2)); break;
-        case 6: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 1, 1>, prm, 512, 2)); break;
-        case 7: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2, 1>, prm, 512, 2)); break;
-        case 8: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0, 1>, prm, 512, 2)); break;
-        case 10: FVB_TRY(coop_launch(c, k_cg<7, 256, 3, 2, 1>, prm, 256, 3)); break;
-        case 11: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 3>, prm)); break;
-        case 12: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;
-        case 13: FVB_TRY(coop_launch(c, k_cg<7, 384, 2, 4>, prm, 384, 2)); break;
-        case 14: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 5>, prm)); break;
-        case 15: FVB_TRY(coop_launch(c, k_cg<7, 256, 4, 4>, prm, 256, 4)); break;
-        case 16: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 6>, prm)); break;
-        case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;
-        case 19: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 1>, prm, 1024, 1)); break;
-        case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;
+        case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;     // plain pass A
+        case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;     // pipelined I/V
+        case 12: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;    // index ring, 2x512
+        case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;  // + ring across barrier
         default: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;
       }
       break;
