@@ -310,6 +310,10 @@ int fvb_team_attach(fvb_ctx* ctx, int rank, int size, void* const* pool_bases,
                     const int64_t* n_cells, int64_t n_inner,
                     const int64_t* send_ptr, const int64_t* send_rank,
                     const int64_t* send_dst);
+/* memory-ordering scope of the team's halo stores and reductions: 1 (the
+ * default after attach) when ranks sit on different devices, 0 when every
+ * rank shares this device (gpu-scope fences suffice) */
+int fvb_team_set_scope(fvb_ctx* ctx, int system_scope);
 /* after every rank attached: make the mesh checks that raise inside a step
  * (coincident centroids, fvm.py:349-370) raise on every rank (team sync) */
 int fvb_team_check(fvb_ctx* ctx);

@@ -21,6 +21,14 @@ from .errors import (
     SparseError,
 )
 
+# Load every kernel when the CUDA context is created.  With lazy loading
+# the first launch of a kernel may wait for the device to drain; ranks of a
+# decomposition that share one device spin-wait on each other inside
+# kernels, so a lazily loaded kernel of one rank could stall behind the
+# other rank's waiting kernel until the watchdog fires.  (Takes effect if
+# CUDA has not been initialised in this process yet.)
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfvb.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -151,6 +159,7 @@ _sig("fvb_ipc_open", I, u8p, C.POINTER(vp))
 _sig("fvb_ipc_close", I, vp)
 _sig("fvb_team_attach", I, vp, I, I, C.POINTER(vp), i64p, I64, i64p, i64p, i64p)
 _sig("fvb_team_check", I, vp)
+_sig("fvb_team_set_scope", I, vp, I)
 _sig("fvb_team_allreduce", I, vp, dp, I, I)
 _sig("fvb_set_sm_share", I, vp, I)
 _sig("fvb_set_bcs", I, vp, I, u8p, i32p, dp, I)
@@ -189,7 +198,7 @@ EXPORTS = [
     "fvb_pattern_plan_create", "fvb_pattern_plan_fill", "fvb_pattern_plan_destroy",
     "fvb_ctx_create", "fvb_ctx_destroy", "fvb_ctx_device_bytes", "fvb_upload_mesh",
     "fvb_upload_mesh_part", "fvb_team_export", "fvb_ipc_open", "fvb_ipc_close",
-    "fvb_team_attach", "fvb_team_check", "fvb_team_allreduce", "fvb_set_sm_share",
+    "fvb_team_attach", "fvb_team_check", "fvb_team_set_scope", "fvb_team_allreduce", "fvb_set_sm_share",
     "fvb_upload_pattern", "fvb_set_bcs", "fvb_set_state", "fvb_get_state", "fvb_op_smvp",
     "fvb_op_stmvp", "fvb_pack_q", "fvb_unpack_q",
     "fvb_mesh_read", "fvb_mesh_read_take", "fvb_mesh_read_free", "fvb_mesh_write",

@@ -42,6 +42,7 @@ int ensure_pool(Ctx* c) {
   T = TeamView{};
   T.rank = 0;
   T.size = 1;
+  T.sys = 0;
   T.comm = reinterpret_cast<Comm*>(p);
   T.peer_comm[0] = T.comm;
   T.peer_cells[0] = c->cells;
@@ -571,10 +572,7 @@ int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_rep
     unsigned err = 0;
     FVB_CUDA(cudaMemcpyAsync(&err, c->sync + 3, sizeof err, cudaMemcpyDeviceToHost, c->stream));
     FVB_CUDA(cudaStreamSynchronize(c->stream));
-    if (err) {
-      fvb_set_error("team sync timed out during the step (rank %d)", c->team.rank);
-      return FVB_E_TIMEOUT;
-    }
+    if (err) return team_timeout_error(c);
   }
   return FVB_OK;
 }
@@ -1329,6 +1327,7 @@ int fvb_team_attach(fvb_ctx* h, int rank, int size, void* const* pool_bases,
     T.peer_nc[q] = int(n_cells[q]);
   }
   T.n_inner = int(n_inner);
+  T.sys = 1;  // until fvb_team_set_scope says all ranks share this device
   const int nsr = c->nr - int(n_inner);
   const int64_t ns = nsr > 0 ? send_ptr[nsr] : 0;
   std::vector<int> sp(size_t(nsr) + 1), sr(static_cast<size_t>(ns)), sd(static_cast<size_t>(ns));
@@ -1371,6 +1370,11 @@ int fvb_team_check(fvb_ctx* h) {
   if (flags[0] > 0 && c->first_zero_dmag < 0) c->first_zero_dmag = 0x7ffffffe;
   for (int f = 0; f < 2; ++f)
     if (flags[1 + f] > 0 && c->first_zero_dbmag_value[f] < 0) c->first_zero_dbmag_value[f] = 0x7ffffffe;
+  return FVB_OK;
+}
+
+int fvb_team_set_scope(fvb_ctx* h, int system_scope) {
+  h->c.team.sys = system_scope ? 1 : 0;
   return FVB_OK;
 }
 

@@ -82,6 +82,7 @@ static_assert(sizeof(Comm) <= kCommBytes, "comm area");
 // Device view of the team: who the peers are and where their pools are.
 struct TeamView {
   int rank, size;             // size 1 = no decomposition
+  int sys;                    // 1: ranks on several devices (system-scope ordering)
   Comm* comm;                 // local comm area
   Comm* peer_comm[kMaxTeam];  // every rank's comm area (own included)
   double* peer_cells[kMaxTeam];  // every rank's slot 0 base
@@ -94,6 +95,21 @@ struct TeamView {
   const int* send_rank;
   const int* send_dst;
 };
+
+// Row ownership of one block in the persistent solvers: rows are
+// grid-strided over every thread (a sweep front that keeps the +-n^2
+// neighbours of the rows in flight L2-resident).  In a team every block may
+// hold send rows, so every arrival is ordered at the team's scope.  (Giving
+// the send rows their own few blocks, so only those arrive at system scope,
+// measured 40% slower per CG iteration on one device: profiles/r01_team.md.)
+struct RowRange {
+  int begin, end, step;
+  bool sends;
+};
+__device__ __forceinline__ RowRange team_rows(const TeamView& T, int nrows) {
+  return RowRange{int(blockIdx.x) * int(blockDim.x) + int(threadIdx.x), nrows,
+                  int(gridDim.x) * int(blockDim.x), T.size > 1 && nrows > T.n_inner};
+}
 
 // Store value v of row i (pool slot `slot`) into the ghost copies held by
 // the ranks that need it.
@@ -359,7 +375,7 @@ __device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
 #pragma unroll
     for (int m = 0; m < M; ++m) pc->mail[par][T.rank][m] = v[m];
   }
-  __threadfence_system();
+  if (T.sys) __threadfence_system(); else __threadfence();
   for (int q = 0; q < T.size; ++q)
     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(&T.peer_comm[q]->seq[T.rank]),
                  "l"(ep)
@@ -370,12 +386,20 @@ __device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
       unsigned long long sq;
       asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(sq) : "l"(&me->seq[q]) : "memory");
       if (sq >= ep) break;
-      if (global_ns() - t0 > kWatchdogNs) return false;
+      if (global_ns() - t0 > kWatchdogNs) {
+        // diagnostics for the host: the epoch waited for and every flag seen
+        me->pad[0] = ep;
+        for (int k = 0; k < T.size && k < 6; ++k) me->pad[1 + k] = me->seq[k];
+        return false;
+      }
     }
   }
   // relaxed reads that observed every flag + fence = acquire (the
   // mailboxes and the peers' halo stores below are current)
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (T.sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
 #pragma unroll
   for (int m = 0; m < M; ++m) {
     const volatile double* box = &me->mail[par][0][m];
@@ -434,11 +458,18 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 template <int M>
 __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
-                                            double* smem /*[32*M+M]*/) {
+                                            double* smem /*[32*M+M]*/, bool sends = true) {
   __shared__ int s_last, s_ok;
   __shared__ unsigned s_gen;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool sys = T.size > 1;
+  // teamed: the result goes through the peer mailboxes (broadcast path);
+  // sys: the peers are other devices, so arrivals order this block's halo
+  // stores at system scope
+  const bool teamed = T.size > 1;
+  // only blocks that stored to peers since the last barrier need their
+  // arrival ordered at system scope (see team_rows); the last arriver's
+  // fence.sys in team_exchange covers the rest through the acq_rel chain
+  const bool sys = teamed && T.sys && sends;
   block_reduce<M>(v, smem);
   volatile unsigned* vabort = sync + 2;
   double* bcast = reinterpret_cast<double*>(sync + 4);
@@ -457,7 +488,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   const unsigned gen = s_gen;
   const double* part = partials + size_t(gen & 1u) * size_t(M) * gridDim.x;
   if (s_last) {
-    if (!sys) {
+    if (!teamed) {
       if (threadIdx.x == 0) {
         sync[0] = 0u;  // reset arrivals; ordered before the release below
         red_release_add(sync + 1, false);
@@ -479,7 +510,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
 #pragma unroll
         for (int m = 0; m < M; ++m) __stcg(bcast + m, r[m]);
         sync[0] = 0u;
-        red_release_add(sync + 1, true);
+        red_release_add(sync + 1, false);  // the waiters are on this device
       }
     }
   } else if (threadIdx.x == 0) {
@@ -497,13 +528,13 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   if (threadIdx.x == 0) {
     ld_acquire_gpu(sync + 1);  // acquire (+ L1 invalidate) before reading results
     s_ok = *vabort == 0;
-    if (sys) {
+    if (teamed) {
 #pragma unroll
       for (int m = 0; m < M; ++m) smem[32 * M + m] = __ldcg(bcast + m);
     }
   }
   __syncthreads();
-  if (!sys && warp == 0) {
+  if (!teamed && warp == 0) {
     // single device: every block sums the partials itself, in the same
     // fixed order (lane-strided over blocks, then a shuffle tree)
 #pragma unroll
@@ -516,7 +547,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     }
     __syncwarp();
   }
-  if (!sys) __syncthreads();
+  if (!teamed) __syncthreads();
 #pragma unroll
   for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
   const bool ok = s_ok != 0;
@@ -559,6 +590,7 @@ std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row
 // and a small allreduce; both are no-ops for a context without a team.
 int team_halo(Ctx* c, int first_slot, int nslots);
 int team_allreduce(Ctx* c, double* host_vals, int m, int op);
+int team_timeout_error(Ctx* c);  // sets the diagnostic error text, returns FVB_E_TIMEOUT
 
 // FV operators on device buffers (fvb_ops.cu); multi-component vectors use
 // component stride nc (the pool layout).

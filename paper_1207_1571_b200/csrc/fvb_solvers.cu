@@ -209,15 +209,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   const TeamView& T = A.T;
   const int nrows = P.n;
   int row0, n, G;
+  bool sends = T.size > 1;
   if (CONTIG) {
     const int chunk = ((nrows + gridDim.x - 1) / gridDim.x + 31) & ~31;
     row0 = blockIdx.x * chunk + threadIdx.x;
     n = min(nrows, (blockIdx.x + 1) * chunk);
     G = blockDim.x;
   } else {
-    row0 = blockIdx.x * blockDim.x + threadIdx.x;
-    n = nrows;
-    G = gridDim.x * blockDim.x;
+    const RowRange R = team_rows(T, nrows);
+    row0 = R.begin;
+    n = R.end;
+    G = R.step;
+    sends = R.sends;
   }
   const int tid = row0;
   const bool team = T.size > 1;
@@ -241,8 +244,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s3[2] += ri * zi;
     }
   }
-  if (!team_reduce<3>(T, A.sync, A.partials, s3, red)) {
-    if (tid == 0) A.result[4] = SE_TIMEOUT;
+  if (!team_reduce<3>(T, A.sync, A.partials, s3, red, sends)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
   const double bnorm = fmax(sqrt(s3[0]), kResFloor);
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       }
     }
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
-    if (!team_reduce<1>(T, A.sync, A.partials, pq, red)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<1>(T, A.sync, A.partials, pq, red, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     // next pass A's first index rows travel while this pass's reduction runs
     if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
     if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
-    if (!team_reduce<2>(T, A.sync, A.partials, s2, red)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<2>(T, A.sync, A.partials, s2, red, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
@@ -321,7 +324,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     slot_new = (slot_new == A.slot_pb) ? A.slot_pa : A.slot_pb;
     first = false;
   }
-  if (tid == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.result[0] = it;
     A.result[1] = conv ? 1.0 : 0.0;
     A.result[2] = res0;
@@ -475,9 +478,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
   __shared__ CompState S[NC];
   const PatternView& P = A.P;
   const TeamView& T = A.T;
-  const int n = P.n;
-  const int G = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const RowRange R = team_rows(T, P.n);
+  const int n = R.end;       // rows of this block: tid, tid + G, ... < n
+  const int G = R.step;
+  const int tid = R.begin;
+  const bool sends = R.sends;
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
   bool act[NC];
@@ -505,8 +510,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
       }
     }
   }
-  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red)) {
-    if (tid == 0)
+  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, sends)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
   }
@@ -584,7 +589,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
     if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
     {
       double z1[1] = {0.0};
-      if (!team_reduce<1>(T, A.sync, A.partials, z1, red)) { timeout = true; break; }
+      if (!team_reduce<1>(T, A.sync, A.partials, z1, red, sends)) { timeout = true; break; }
     }
     if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
     // pass V: v = A p_hat, r_hat.v
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red)) { timeout = true; break; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -643,7 +648,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, ss, red)) { timeout = true; break; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, ss, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -690,7 +695,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red)) { timeout = true; break; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -724,7 +729,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red)) { timeout = true; break; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -738,7 +743,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
       __syncthreads();
     }
   }
-  if (tid == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int c = 0; c < NC; ++c) {
       A.result[6 * c + 0] = S[c].it;
       A.result[6 * c + 1] = S[c].done ? 1.0 : 0.0;
@@ -792,9 +797,11 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
   __shared__ CompState S[NC];
   const PatternView& P = A.P;
   const TeamView& T = A.T;
-  const int n = P.n;
-  const int G = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const RowRange R = team_rows(T, P.n);
+  const int n = R.end;       // rows of this block: tid, tid + G, ... < n
+  const int G = R.step;
+  const int tid = R.begin;
+  const bool sends = R.sends;
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
   bool act[NC];
@@ -826,8 +833,8 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
       }
     }
   }
-  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red)) {
-    if (tid == 0)
+  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, sends)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
   }
@@ -934,7 +941,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red)) { timeout = true; break; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -981,7 +988,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<3 * NC>(T, A.sync, A.partials, st, red)) { timeout = true; break; }
+      if (!team_reduce<3 * NC>(T, A.sync, A.partials, st, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -1036,7 +1043,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red)) { timeout = true; break; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -1053,7 +1060,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
     }
     cur = nxt;
   }
-  if (tid == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int c = 0; c < NC; ++c) {
       A.result[6 * c + 0] = S[c].it;
       A.result[6 * c + 1] = S[c].done ? 1.0 : 0.0;
@@ -1077,7 +1084,10 @@ int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
     return FVB_E_CUDA;
   }
   if (per_sm > max_per_sm) per_sm = max_per_sm;
-  const int b = per_sm * c->num_sms / (c->sm_share > 0 ? c->sm_share : 1);
+  // ranks sharing one device (tests): each takes 1/share of the SMs, with
+  // `share` SMs left over for the other ranks' one-block sync kernels
+  const int share = c->sm_share > 0 ? c->sm_share : 1;
+  const int b = share > 1 ? per_sm * (c->num_sms - share) / share : per_sm * c->num_sms;
   *blocks = b < 1 ? 1 : b;
   return FVB_OK;
 }

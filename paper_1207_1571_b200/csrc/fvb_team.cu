@@ -4,6 +4,8 @@
 // allreduce through the peer mailboxes.  The domain decomposition itself
 // (which rows send where) is built on the host (decompose.py) and handed
 // over by fvb_team_attach.
+#include <cstddef>
+
 #include "fvb_internal.cuh"
 
 namespace fvb {
@@ -43,6 +45,21 @@ __global__ void k_team_sync(TeamView T, double* vals, int m, int op, unsigned* e
 
 }  // namespace
 
+int team_timeout_error(Ctx* c) {
+  unsigned long long d[8] = {0};
+  cudaMemcpy(d, reinterpret_cast<const char*>(c->pool) + offsetof(Comm, pad), 7 * sizeof(d[0]),
+             cudaMemcpyDeviceToHost);
+  unsigned long long seq[kMaxTeam] = {0};
+  cudaMemcpy(seq, c->pool, sizeof seq, cudaMemcpyDeviceToHost);
+  char peers[256] = {0};
+  int o = 0;
+  for (int q = 0; q < c->team.size && q < kMaxTeam; ++q)
+    o += snprintf(peers + o, sizeof peers - o, "%s%llu", q ? "," : "", seq[q]);
+  fvb_set_error("team sync timed out (rank %d of %d): a peer did not arrive (waited for epoch "
+                "%llu; peer epochs now %s)", c->team.rank, c->team.size, d[0], peers);
+  return FVB_E_TIMEOUT;
+}
+
 int team_halo(Ctx* c, int first_slot, int nslots) {
   if (!c->teamed()) return FVB_OK;
   const int nsend = c->nr - c->team.n_inner;
@@ -75,11 +92,7 @@ int team_allreduce(Ctx* c, double* host_vals, int m, int op) {
   FVB_CUDA(cudaMemcpyAsync(host_vals, dv, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaMemcpyAsync(&err, c->sync + 3, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
-  if (err) {
-    fvb_set_error("team sync timed out (rank %d of %d): a peer did not arrive", c->team.rank,
-                  c->team.size);
-    return FVB_E_TIMEOUT;
-  }
+  if (err) return team_timeout_error(c);
   return FVB_OK;
 }
 

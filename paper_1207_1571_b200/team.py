@@ -23,6 +23,7 @@ and gather u, p, flux back into global order on request.
 
 import ctypes as C
 import os
+import socket
 import threading
 
 import numpy as np
@@ -122,6 +123,15 @@ class _LocalField:
         self.rank = field.rank
 
 
+def _scope(same_device):
+    """System-scope ordering unless every rank shares one device;
+    FVB_TEAM_SCOPE=sys|gpu overrides (experiments)."""
+    env = os.environ.get("FVB_TEAM_SCOPE")
+    if env in ("sys", "gpu"):
+        return 1 if env == "sys" else 0
+    return 0 if same_device else 1
+
+
 def _speeds(u_field, geom, t):
     """Per-patch normal speeds of timed / mass-flow inlets, from the GLOBAL
     geometry (the mass-flow area is the whole patch's, fvm.py:187-193)."""
@@ -203,6 +213,11 @@ class DecomposedRun(_TeamRunBase):
         if devices is None:
             devices = [device_index()] * self.nparts
         share = max(devices.count(d) for d in set(devices))
+        if share > 4:
+            # ranks sharing one device spin-wait on each other inside kernels;
+            # beyond 4 per device the scheduler can starve a waiting rank
+            raise ValueError(f"{share} ranks on one device (at most 4 are supported; "
+                             "use one device per rank for larger teams)")
         self.members = []
         for r in range(self.nparts):
             sd = build_subdomain(mesh, self.pattern, part, r, topo)
@@ -210,8 +225,11 @@ class DecomposedRun(_TeamRunBase):
         ex = [m.export() for m in self.members]
         bases = [e[0] for e in ex]
         ncs = [e[1] for e in ex]
+        same_device = len(set(devices)) == 1
+        scope = _scope(same_device)
         for m in self.members:  # allocations + copies: no team sync inside
             _lib.check(m.attach(bases, ncs))
+            _lib.check(_lib.lib.fvb_team_set_scope(m.ctx.h, scope))
         self._parallel(lambda m: _lib.lib.fvb_team_check(m.ctx.h))
         for m in self.members:
             m.set_bcs(self.u_field, self.p_field, self.geom)
@@ -327,10 +345,10 @@ class RankRun(_TeamRunBase):
         share = int(os.environ.get("FVB_SM_SHARE", "1"))
         self.member = _Member(sd, self.geom, mesh.n_internal, device, share)
         base, nc, handle = self.member.export()
-        infos = allgather((os.getpid(), device, base, nc, handle))
+        infos = allgather((os.getpid(), device, base, nc, handle, socket.gethostname()))
         self._opened = []
         bases = []
-        for q, (pid, dev, b, ncq, h) in enumerate(infos):
+        for q, (pid, dev, b, ncq, h, _host) in enumerate(infos):
             if q == rank:
                 bases.append(base)
             elif pid == os.getpid():
@@ -342,6 +360,8 @@ class RankRun(_TeamRunBase):
                 self._opened.append(ptr.value)
                 bases.append(ptr.value)
         _lib.check(self.member.attach(bases, [i[3] for i in infos]))
+        same_device = len({(i[5], i[1]) for i in infos}) == 1
+        _lib.check(_lib.lib.fvb_team_set_scope(self.member.ctx.h, _scope(same_device)))
         _lib.check(_lib.lib.fvb_team_check(self.member.ctx.h))
         self.member.set_bcs(self.u_field, self.p_field, self.geom)
         n = mesh.n_cells
