@@ -466,10 +466,21 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   // sys: the peers are other devices, so arrivals order this block's halo
   // stores at system scope
   const bool teamed = T.size > 1;
-  // only blocks that stored to peers since the last barrier need their
-  // arrival ordered at system scope (see team_rows); the last arriver's
-  // fence.sys in team_exchange covers the rest through the acq_rel chain
+  // Arrivals are ordered at GPU scope even in a multi-device team: a block's
+  // halo stores to peers precede its acq_rel.gpu arrival, that arrival
+  // precedes the last arriver's acquire, and the last arriver's fence.sc.sys
+  // before the mailbox flags is cumulative over everything in its causal
+  // past — so every halo store is visible to a peer that acquired the flag
+  // (PTX memory model: causality order is transitive across scopes).  A
+  // system-scope arrival for every block measured ~6 us more per reduction
+  // (profiles/r01_team.md).  FVB_TEAM_SCOPE=sys on the host plus
+  // FVB_ARRIVE_SYS=1 at build time restores it.
+#ifdef FVB_ARRIVE_SYS
   const bool sys = teamed && T.sys && sends;
+#else
+  const bool sys = false;
+  (void)sends;
+#endif
   block_reduce<M>(v, smem);
   volatile unsigned* vabort = sync + 2;
   double* bcast = reinterpret_cast<double*>(sync + 4);
