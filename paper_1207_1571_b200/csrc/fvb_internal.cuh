@@ -458,10 +458,60 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 template <int M>
 __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
-                                            double* smem /*[32*M+M]*/, bool sends = true) {
+                                            double* smem /*[32*M+M]*/, unsigned& rnd,
+                                            bool sends = true) {
   __shared__ int s_last, s_ok;
   __shared__ unsigned s_gen;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (T.size <= 1) {
+    // One device: a monotonic arrival counter, no last-arriver hand-off.
+    // Every block publishes its partials, arrives with a release add and
+    // waits until all gridDim.x blocks of round rnd arrived, then sums the
+    // partials itself in the fixed order (identical in every block).
+    // Partials are double-buffered by round parity: a block writes round
+    // r+2 only after passing round r+1, i.e. after every block finished
+    // reading round r.
+    (void)sends;
+    block_reduce<M>(v, smem);
+    const unsigned r = rnd++;
+    double* part = partials + size_t(r & 1u) * size_t(M) * gridDim.x;
+    volatile unsigned* vabort = sync + 2;
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) part[size_t(m) * gridDim.x + blockIdx.x] = v[m];
+      red_release_add(sync, false);
+      const unsigned target = (r + 1u) * gridDim.x;
+      const uint64_t t0 = global_ns();
+      int spins = 0;
+      while (ld_relaxed_gpu(sync) < target) {
+        if (*vabort) break;
+        if (++spins > 64) __nanosleep(32);
+        if ((spins & 1023) == 0 && global_ns() - t0 > kWatchdogNs) {
+          atomicExch(sync + 2, 1u);
+          break;
+        }
+      }
+      ld_acquire_gpu(sync);  // acquire (+ L1 invalidate) before reading results
+      s_ok = *vabort == 0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double x = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(part + size_t(m) * gridDim.x + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) smem[32 * M + m] = x;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
+    const bool ok = s_ok != 0;
+    __syncthreads();
+    return ok;
+  }
   // teamed: the result goes through the peer mailboxes (broadcast path);
   // sys: the peers are other devices, so arrivals order this block's halo
   // stores at system scope

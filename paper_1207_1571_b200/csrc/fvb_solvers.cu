@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   const int nrows = P.n;
   int row0, n, G;
   bool sends = T.size > 1;
+  unsigned rnd = 0;  // reduction round of this launch (team_reduce)
   if (CONTIG) {
     const int chunk = ((nrows + gridDim.x - 1) / gridDim.x + 31) & ~31;
     row0 = blockIdx.x * chunk + threadIdx.x;
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s3[2] += ri * zi;
     }
   }
-  if (!team_reduce<3>(T, A.sync, A.partials, s3, red, sends)) {
+  if (!team_reduce<3>(T, A.sync, A.partials, s3, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       }
     }
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
-    if (!team_reduce<1>(T, A.sync, A.partials, pq, red, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<1>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     // next pass A's first index rows travel while this pass's reduction runs
     if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
     if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
-    if (!team_reduce<2>(T, A.sync, A.partials, s2, red, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<2>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
   const int G = R.step;
   const int tid = R.begin;
   const bool sends = R.sends;
+  unsigned rnd = 0;  // reduction round of this launch (team_reduce)
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
   bool act[NC];
@@ -510,7 +512,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
       }
     }
   }
-  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, sends)) {
+  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
     if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
     {
       double z1[1] = {0.0};
-      if (!team_reduce<1>(T, A.sync, A.partials, z1, red, sends)) { timeout = true; break; }
+      if (!team_reduce<1>(T, A.sync, A.partials, z1, red, rnd, sends)) { timeout = true; break; }
     }
     if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
     // pass V: v = A p_hat, r_hat.v
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, sends)) { timeout = true; break; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, ss, red, sends)) { timeout = true; break; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, ss, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -729,7 +731,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -802,6 +804,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
   const int G = R.step;
   const int tid = R.begin;
   const bool sends = R.sends;
+  unsigned rnd = 0;  // reduction round of this launch (team_reduce)
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
   bool act[NC];
@@ -833,7 +836,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
       }
     }
   }
-  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, sends)) {
+  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
@@ -941,7 +944,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, sends)) { timeout = true; break; }
+      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -988,7 +991,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<3 * NC>(T, A.sync, A.partials, st, red, sends)) { timeout = true; break; }
+      if (!team_reduce<3 * NC>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -1043,7 +1046,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
