@@ -202,7 +202,7 @@ __device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double
 // gives every block one contiguous chunk swept in blockDim steps, so the
 // +-1 and +-n neighbours a row gathers were loaded by the same SM moments
 // earlier (L1 hits) and only the +-n^2 ones come from L2.
-template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0>
+template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0, int PB2 = 0>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
   const PatternView& P = A.P;
@@ -226,6 +226,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   const int tid = row0;
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
+  const bool vec_ok = PB2 && ((reinterpret_cast<uintptr_t>(A.pb) | reinterpret_cast<uintptr_t>(A.pa) |
+                               reinterpret_cast<uintptr_t>(A.x) | reinterpret_cast<uintptr_t>(A.r) |
+                               reinterpret_cast<uintptr_t>(A.q) | reinterpret_cast<uintptr_t>(A.z) |
+                               reinterpret_cast<uintptr_t>(inv)) & 15u) == 0;
 
   // setup: r = b - A x0, z = r / D, ||b||, ||r||, r.z  (linsolve.py:106-127)
   double s3[3] = {0.0, 0.0, 0.0};
@@ -300,7 +304,39 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     const double alpha = rz / pq[0];
     // pass B: x += alpha p, r -= alpha q, z = r / D, ||r||^2, r.z
     double s2[2] = {0.0, 0.0};
-    for (int i = tid; i < n; i += G) {
+    int i_scalar = tid;
+    if (PB2 && !CONTIG && vec_ok) {
+      // two consecutive rows per thread with 16-byte loads/stores
+      const int npair = n >> 1;
+      for (int j = tid; j < npair; j += G) {
+        const int i = 2 * j;
+        const double2 pv = __ldcg(reinterpret_cast<const double2*>(pnew + i));
+        const double2 xv = __ldcg(reinterpret_cast<const double2*>(A.x + i));
+        const double2 rv = __ldcg(reinterpret_cast<const double2*>(A.r + i));
+        const double2 qv = __ldcg(reinterpret_cast<const double2*>(A.q + i));
+        const double2 iv = __ldcg(reinterpret_cast<const double2*>(inv + i));
+        double2 xo, ro, zo;
+        xo.x = xv.x + alpha * pv.x;
+        xo.y = xv.y + alpha * pv.y;
+        ro.x = rv.x - alpha * qv.x;
+        ro.y = rv.y - alpha * qv.y;
+        zo.x = ro.x * iv.x;
+        zo.y = ro.y * iv.y;
+        *reinterpret_cast<double2*>(A.x + i) = xo;
+        *reinterpret_cast<double2*>(A.r + i) = ro;
+        *reinterpret_cast<double2*>(A.z + i) = zo;
+        if (team && i + 1 >= T.n_inner) {
+          if (i >= T.n_inner) halo_send(T, i, A.slot_z, zo.x);
+          halo_send(T, i + 1, A.slot_z, zo.y);
+        }
+        s2[0] += ro.x * ro.x;
+        s2[1] += ro.x * zo.x;
+        s2[0] += ro.y * ro.y;
+        s2[1] += ro.y * zo.y;
+      }
+      i_scalar = 2 * npair + tid;  // odd tail row
+    }
+    for (int i = i_scalar; i < n; i += G) {
       const double pi = pnew[i];
       A.x[i] = A.x[i] + alpha * pi;
       const double ri = A.r[i] - alpha * A.q[i];
@@ -1193,20 +1229,22 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   // experiments, tools/cg_micro.py); the default is the measured best:
   // pass A with the column indices prefetched two rows ahead (the gather's
   // address chain), evict-first matrix loads, grid-strided rows, one
-  // 1024-thread block per SM (profiles/r01_cg_variants.md).
+  // 1024-thread block per SM, pass B on row pairs with 16-byte L2-only
+  // loads (profiles/r01_cg_variants.md).
   static const int variant = [] {
     const char* e = getenv("FVB_CG_VARIANT");
     return e ? atoi(e) : -1;
   }();
   switch (c->k) {
-    case 5: FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4>, prm, 1024, 1)); break;
+    case 5: FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;
     case 7:
       switch (variant) {
         case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;     // plain pass A
         case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;     // pipelined I/V
         case 12: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;    // index ring, 2x512
         case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;  // + ring across barrier
-        default: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;
+        case 17: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;  // scalar pass B
+        default: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;
       }
       break;
     default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
