@@ -846,6 +846,14 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
   bool act[NC];
   bool timeout = false;
   constexpr int KR = KT > 0 ? KT : 1;
+  uintptr_t al_or = reinterpret_cast<uintptr_t>(inv);
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+    al_or |= reinterpret_cast<uintptr_t>(A.x[c]) | reinterpret_cast<uintptr_t>(A.r[c]) |
+             reinterpret_cast<uintptr_t>(A.rh[c]) | reinterpret_cast<uintptr_t>(A.t[c]) |
+             reinterpret_cast<uintptr_t>(A.p[0][c]) | reinterpret_cast<uintptr_t>(A.p[1][c]) |
+             reinterpret_cast<uintptr_t>(A.v[0][c]) | reinterpret_cast<uintptr_t>(A.v[1][c]);
+  const bool vec_ok = (al_or & 15u) == 0;
 
   // setup (linsolve.py:180-196): r = b - A x0, r_hat = r, ||b||, ||r||
   double sums[2 * NC];
@@ -1060,7 +1068,46 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         al[c] = S[c].alpha;
         om[c] = S[c].omega;
       }
-      for (int i = tid; i < n; i += G) {
+      int i_scalar = tid;
+      if (vec_ok) {
+        // row pairs, 16-byte L2-only loads and 16-byte stores (as CG pass B)
+        const int npair = n >> 1;
+        for (int j = tid; j < npair; j += G) {
+          const int i = 2 * j;
+          const double2 iv = __ldcg(reinterpret_cast<const double2*>(inv + i));
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (!xa[c]) continue;
+            const double2 pv = __ldcg(reinterpret_cast<const double2*>(A.p[nxt][c] + i));
+            const double2 xv = __ldcg(reinterpret_cast<const double2*>(A.x[c] + i));
+            double2 xo;
+            xo.x = xv.x + al[c] * (pv.x * iv.x);
+            xo.y = xv.y + al[c] * (pv.y * iv.y);
+            if (full[c]) {
+              const double2 rv = __ldcg(reinterpret_cast<const double2*>(A.r[c] + i));
+              const double2 vv = __ldcg(reinterpret_cast<const double2*>(A.v[nxt][c] + i));
+              const double2 tv = __ldcg(reinterpret_cast<const double2*>(A.t[c] + i));
+              const double2 hv = __ldcg(reinterpret_cast<const double2*>(A.rh[c] + i));
+              const double s0 = rv.x - al[c] * vv.x, s1 = rv.y - al[c] * vv.y;
+              xo.x = xo.x + om[c] * (s0 * iv.x);
+              xo.y = xo.y + om[c] * (s1 * iv.y);
+              const double r0 = s0 - om[c] * tv.x, r1 = s1 - om[c] * tv.y;
+              *reinterpret_cast<double2*>(A.r[c] + i) = make_double2(r0, r1);
+              if (team && i + 1 >= T.n_inner) {
+                if (i >= T.n_inner) halo_send(T, i, A.slot_r[c], r0);
+                halo_send(T, i + 1, A.slot_r[c], r1);
+              }
+              rr[2 * c] += r0 * r0;
+              rr[2 * c + 1] += hv.x * r0;
+              rr[2 * c] += r1 * r1;
+              rr[2 * c + 1] += hv.y * r1;
+            }
+            *reinterpret_cast<double2*>(A.x[c] + i) = xo;
+          }
+        }
+        i_scalar = 2 * npair + tid;
+      }
+      for (int i = i_scalar; i < n; i += G) {
         const double iv = inv[i];
         const bool snd = team && i >= T.n_inner;
 #pragma unroll

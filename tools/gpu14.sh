@@ -1,3 +1,2 @@
-timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -4
-timeout 1500 python bench.py --no-cpu-baseline --no-e2e 2>&1 | tail -c 700
-FVB_BI_VARIANT=5 timeout 1500 python bench.py --no-cpu-baseline --no-e2e 2>&1 | tail -c 400
+timeout 1500 python -m pytest tests/test_gpu_solvers.py tests/test_gpu_coupling.py tests/test_gpu_configs.py tests/test_gpu_team.py -q -x 2>&1 | tail -2
+timeout 1500 python bench.py --no-cpu-baseline --no-e2e --no-aux 2>&1 | tail -c 900
