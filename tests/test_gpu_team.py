@@ -110,7 +110,7 @@ def test_ipc_team_two_processes_one_device():
     env = dict(os.environ, FVB_DEVICE="0", FVB_SM_SHARE="2")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(here, "tools", "ipc_team_check.py"), "6"]
+           os.path.join(here, "tools", "ipc_team_check.py"), "4"]
     out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=300, cwd=here)
     assert out.returncode == 0, out.stderr[-2000:]
     line = [ln for ln in out.stdout.splitlines() if ln.startswith("IPC team of 2")]
