@@ -903,7 +903,12 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
 
   uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
   const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
-  int cur = 0;  // p[cur], v[cur]: previous iteration; p[nxt], v[nxt]: this one
+  // p (own rows), v, and d = p - omega v stored by pass 3 for the next pass 1,
+  // so pass 1 gathers r and d only (the reference's p = r + beta (p - omega v)
+  // with the inner difference rounded once, as it is there)
+  double* const* Pp = A.p[0];
+  double* const* Pv = A.v[0];
+  double* const* Pd = A.p[1];
   while (!timeout) {
     if (timer) tk = global_ns();
     if (threadIdx.x == 0) {
@@ -933,7 +938,6 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
       any = any || act[c];
     }
     if (!any) break;
-    const int nxt = cur ^ 1;
     // pass 1: p = r | r + beta (p - omega v); v = A (p / D) rebuilt per
     // gathered column; r_hat.v
     {
@@ -951,9 +955,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
       auto pval = [&](int c, int col) {
         const double ri = A.r[c][col];
         if (cp[c]) return ri;
-        double pi = A.p[cur][c][col] - om[c] * A.v[cur][c][col];
-        pi = pi * be[c];
-        return pi + ri;
+        return Pd[c][col] * be[c] + ri;
       };
       auto g = [&](int c, int col) { return pval(c, col) * inv[col]; };
       auto body = [&](int i, const double* y) {
@@ -962,8 +964,8 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         for (int c = 0; c < NC; ++c) {
           if (!act[c]) continue;
           const double pi = pval(c, i);
-          A.p[nxt][c][i] = pi;
-          A.v[nxt][c][i] = y[c];
+          Pp[c][i] = pi;
+          Pv[c][i] = y[c];
           double rhi;
           if (S[c].restart) {
             rhi = A.r[c][i];
@@ -972,8 +974,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
             rhi = A.rh[c][i];
           }
           if (snd) {
-            halo_send(T, i, A.slot_p[nxt][c], pi);
-            halo_send(T, i, A.slot_v[nxt][c], y[c]);
+            halo_send(T, i, A.slot_v[0][c], y[c]);
           }
           rv[c] += rhi * y[c];
         }
@@ -1009,7 +1010,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
       double al[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) al[c] = S[c].alpha;
-      auto sval = [&](int c, int col) { return A.r[c][col] - al[c] * A.v[nxt][c][col]; };
+      auto sval = [&](int c, int col) { return A.r[c][col] - al[c] * Pv[c][col]; };
       auto g = [&](int c, int col) { return sval(c, col) * inv[col]; };
       auto body = [&](int i, const double* y) {
 #pragma unroll
@@ -1078,24 +1079,30 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
 #pragma unroll
           for (int c = 0; c < NC; ++c) {
             if (!xa[c]) continue;
-            const double2 pv = __ldcg(reinterpret_cast<const double2*>(A.p[nxt][c] + i));
+            const double2 pv = __ldcg(reinterpret_cast<const double2*>(Pp[c] + i));
             const double2 xv = __ldcg(reinterpret_cast<const double2*>(A.x[c] + i));
             double2 xo;
             xo.x = xv.x + al[c] * (pv.x * iv.x);
             xo.y = xv.y + al[c] * (pv.y * iv.y);
             if (full[c]) {
               const double2 rv = __ldcg(reinterpret_cast<const double2*>(A.r[c] + i));
-              const double2 vv = __ldcg(reinterpret_cast<const double2*>(A.v[nxt][c] + i));
+              const double2 vv = __ldcg(reinterpret_cast<const double2*>(Pv[c] + i));
               const double2 tv = __ldcg(reinterpret_cast<const double2*>(A.t[c] + i));
               const double2 hv = __ldcg(reinterpret_cast<const double2*>(A.rh[c] + i));
               const double s0 = rv.x - al[c] * vv.x, s1 = rv.y - al[c] * vv.y;
               xo.x = xo.x + om[c] * (s0 * iv.x);
               xo.y = xo.y + om[c] * (s1 * iv.y);
               const double r0 = s0 - om[c] * tv.x, r1 = s1 - om[c] * tv.y;
+              const double d0 = pv.x - om[c] * vv.x, d1 = pv.y - om[c] * vv.y;
               *reinterpret_cast<double2*>(A.r[c] + i) = make_double2(r0, r1);
+              *reinterpret_cast<double2*>(Pd[c] + i) = make_double2(d0, d1);
               if (team && i + 1 >= T.n_inner) {
-                if (i >= T.n_inner) halo_send(T, i, A.slot_r[c], r0);
+                if (i >= T.n_inner) {
+                  halo_send(T, i, A.slot_r[c], r0);
+                  halo_send(T, i, A.slot_p[1][c], d0);
+                }
                 halo_send(T, i + 1, A.slot_r[c], r1);
+                halo_send(T, i + 1, A.slot_p[1][c], d1);
               }
               rr[2 * c] += r0 * r0;
               rr[2 * c + 1] += hv.x * r0;
@@ -1113,15 +1120,22 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           if (!xa[c]) continue;
-          const double phi = A.p[nxt][c][i] * iv;
+          const double pi = Pp[c][i];
+          const double phi = pi * iv;
           double xi = A.x[c][i] + al[c] * phi;
           if (full[c]) {
-            const double si = A.r[c][i] - al[c] * A.v[nxt][c][i];
+            const double vi = Pv[c][i];
+            const double si = A.r[c][i] - al[c] * vi;
             const double shi = si * iv;
             xi = xi + om[c] * shi;
             const double ri = si - om[c] * A.t[c][i];
+            const double di = pi - om[c] * vi;
             A.r[c][i] = ri;
-            if (snd) halo_send(T, i, A.slot_r[c], ri);
+            Pd[c][i] = di;
+            if (snd) {
+              halo_send(T, i, A.slot_r[c], ri);
+              halo_send(T, i, A.slot_p[1][c], di);
+            }
             rr[2 * c] += ri * ri;
             rr[2 * c + 1] += A.rh[c][i] * ri;
           }
@@ -1144,7 +1158,6 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       __syncthreads();
     }
-    cur = nxt;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int c = 0; c < NC; ++c) {
