@@ -473,6 +473,19 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     // reading round r.
     (void)sends;
     block_reduce<M>(v, smem);
+    if (gridDim.x == 1) {
+      // small systems run on a single block: the block barrier is the grid barrier
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) smem[32 * M + m] = v[m];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
+      __syncthreads();
+      ++rnd;
+      return true;
+    }
     const unsigned r = rnd++;
     double* part = partials + size_t(r & 1u) * size_t(M) * gridDim.x;
     volatile unsigned* vabort = sync + 2;

@@ -1186,7 +1186,10 @@ int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   // ranks sharing one device (tests): each takes 1/share of the SMs, with
   // `share` SMs left over for the other ranks' one-block sync kernels
   const int share = c->sm_share > 0 ? c->sm_share : 1;
-  const int b = share > 1 ? per_sm * (c->num_sms - share) / share : per_sm * c->num_sms;
+  int b = share > 1 ? per_sm * (c->num_sms - share) / share : per_sm * c->num_sms;
+  // small systems: one block (block barriers instead of grid barriers) while
+  // the rows per thread stay low
+  if (!c->teamed() && c->nr <= 4 * threads) b = 1;
   *blocks = b < 1 ? 1 : b;
   return FVB_OK;
 }

@@ -1,0 +1,34 @@
+"""Small-mesh timing (BASELINE configs[0] C1: 2D cavity 20x20, 100 PISO
+steps; and C3 BFS nh=16 SIMPLE): wall seconds per step on the device path."""
+import json, os, sys, time
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+from paper_1207_1571_b200 import cases
+from paper_1207_1571_b200.cases import Case
+from paper_1207_1571_b200.config import BoundarySpec, CaseConfig
+from paper_1207_1571_b200.coupling import CouplingConfig, init_state, piso_time_step, simple_outer_iteration
+
+m = cases.box_mesh(20, 20, 1, 0.1, 0.1, 0.01, [("movingWall", "wall", ["y+"]), ("fixedWalls", "wall", ["x-", "x+", "y-"]), ("frontAndBack", "empty", ["z-", "z+"])])
+cc = CaseConfig(); cc.nu, cc.algorithm, cc.dt, cc.end_time = 0.01, "piso", 0.005, 0.5
+cc.boundary = {"movingWall": BoundarySpec(u=("fixed_value", (1.0, 0.0, 0.0)), p=("zero_gradient",)),
+               "fixedWalls": BoundarySpec(u=("no_slip",), p=("zero_gradient",)),
+               "frontAndBack": BoundarySpec(u=("empty",), p=("empty",))}
+case = Case("c1", m, cc)
+cfg = CouplingConfig.from_case_config(cc)
+st = init_state(case, cfg)
+piso_time_step(st, cfg)
+t0 = time.perf_counter()
+for _ in range(99):
+    piso_time_step(st, cfg)
+dt = (time.perf_counter() - t0) / 99
+print(json.dumps({"case": "C1 cavity 20x20x1 PISO", "ms_per_step": 1e3 * dt,
+                  "cg_iters_per_step": st.cum_iters["cg"] / 100, "reference_ms_per_step": 7.4}))
+case = cases.gen_backward_step(16)
+cfg = CouplingConfig.from_case_config(case.config)
+st = init_state(case, cfg)
+simple_outer_iteration(st, cfg)
+t0 = time.perf_counter()
+for _ in range(20):
+    simple_outer_iteration(st, cfg)
+dt = (time.perf_counter() - t0) / 20
+print(json.dumps({"case": "C3 BFS nh=16 SIMPLE", "ms_per_sweep": 1e3 * dt,
+                  "cg_iters_per_sweep": st.cum_iters["cg"] / 21, "reference_ms_per_sweep": 689}))
