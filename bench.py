@@ -369,6 +369,48 @@ def measure_c2(steps, warmup):
             "cg_iters_per_step": sum(it for it, _ in cg) / steps}
 
 
+def measure_small():
+    """BASELINE configs[0] (C1: 2D cavity 20x20x1, 100 PISO steps, dt 0.005)
+    and configs[2] at the parity size (C3: backward-facing step nh = 16,
+    SIMPLE): host wall time per step through the public API, next to the
+    reference's own timings on an 8-core host (7.4 ms per C1
+    step, 689 ms per C3 nh=16 sweep)."""
+    from paper_1207_1571_b200 import cases
+    from paper_1207_1571_b200.cases import Case
+    from paper_1207_1571_b200.config import BoundarySpec, CaseConfig
+    from paper_1207_1571_b200.coupling import (CouplingConfig, init_state, piso_time_step,
+                                               simple_outer_iteration)
+
+    m = cases.box_mesh(20, 20, 1, 0.1, 0.1, 0.01,
+                       [("movingWall", "wall", ["y+"]), ("fixedWalls", "wall", ["x-", "x+", "y-"]),
+                        ("frontAndBack", "empty", ["z-", "z+"])])
+    cc = CaseConfig()
+    cc.nu, cc.algorithm, cc.dt, cc.end_time = 0.01, "piso", 0.005, 0.5
+    cc.boundary = {
+        "movingWall": BoundarySpec(u=("fixed_value", (1.0, 0.0, 0.0)), p=("zero_gradient",)),
+        "fixedWalls": BoundarySpec(u=("no_slip",), p=("zero_gradient",)),
+        "frontAndBack": BoundarySpec(u=("empty",), p=("empty",))}
+    cfg = CouplingConfig.from_case_config(cc)
+    st = init_state(Case("c1", m, cc), cfg)
+    t0 = time.perf_counter()
+    for _ in range(100):
+        piso_time_step(st, cfg)
+    c1 = (time.perf_counter() - t0) / 100
+    case = cases.gen_backward_step(16)
+    cfg = CouplingConfig.from_case_config(case.config)
+    st3 = init_state(case, cfg)
+    simple_outer_iteration(st3, cfg)
+    t0 = time.perf_counter()
+    for _ in range(20):
+        simple_outer_iteration(st3, cfg)
+    c3 = (time.perf_counter() - t0) / 20
+    return {"c1_cavity2d_20x20": {"ms_per_step": 1e3 * c1, "steps": 100,
+                                  "cg_iters_per_step": st.cum_iters["cg"] / 100,
+                                  "reference_ms_per_step_surveyed": 7.4},
+            "c3_bfs_nh16": {"ms_per_sweep": 1e3 * c3, "sweeps": 20, "cells": case.mesh.n_cells,
+                            "reference_ms_per_sweep_surveyed": 689.0}}
+
+
 def run_ours(args):
     import ctypes as C
 
@@ -507,9 +549,11 @@ def run_ours(args):
                               f"OpenBLAS default threads; {d['sample_s']:.1f} s of CPU work"),
                    "s_per_step": d["s_per_step"]}
     # ------------------------------------------- auxiliary C2 (configs[1])
-    aux = None
+    aux = aux_small = None
     if D.world == 1 and n != 128 and not args.no_aux:
         aux = measure_c2(steps=3, warmup=2)
+    if D.world == 1 and not args.no_aux:
+        aux_small = measure_small()
     out = {
         "metric": METRIC,
         "value": N / (ms_step / 1e3),
@@ -551,6 +595,7 @@ def run_ours(args):
         "clocks": clk,
         "cpu_baseline": cpu,
         "aux_c2_128": aux,
+        "aux_small": aux_small,
     }
     if D.rank == 0:
         print(json.dumps(out))
