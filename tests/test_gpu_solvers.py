@@ -143,3 +143,65 @@ def test_stage_times_from_device_timers():
     assert sum(st.values()) <= rep.wall_time * 1.000001 + 1e-9
     x, rep = cg(A, g["in_b"], np.zeros(n), SolveConfig(tolerance=1e-10, max_iters=5000))
     assert rep.stage_times == {}
+
+
+def _box_operator(n, crs_tail, rng):
+    from paper_1207_1571_b200 import cases
+    mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
+    ni = mesh.n_internal
+    pairs = np.stack([np.asarray(mesh.owner[:ni]), np.asarray(mesh.neighbour)], axis=1)
+    N = mesh.n_cells
+    if crs_tail:
+        # long-range couplings on ~2% of the rows with K capped at 7: the
+        # overflow entries go to the CRS tail
+        a = rng.choice(N, size=N // 50, replace=False)
+        b = (a + N // 3 + 7) % N
+        extra = np.stack([np.minimum(a, b), np.maximum(a, b)], axis=1)
+        pairs = np.unique(np.concatenate([pairs, extra[extra[:, 0] != extra[:, 1]]]), axis=0)
+    p = sparse.pattern_from_pairs(N, pairs, 7)
+    A = sparse.HybridMatrix.zeros(p)
+    rows = np.arange(N)[:, None]
+    A.V[:] = np.where(p.I >= 0, np.where(p.I > rows, -0.6, -1.4) * rng.uniform(0.5, 1.5, p.I.shape), 0.0)
+    A.V[np.arange(N), p.diag_slot] = 0.0
+    dense_rows = [np.repeat(np.arange(N), p.k)[p.I.ravel() >= 0]]
+    dense_cols = [p.I.ravel()[p.I.ravel() >= 0]]
+    vals = [A.V.ravel()[p.I.ravel() >= 0]]
+    if p.nnz_crs:
+        A.crs_val[:] = -0.3 * rng.uniform(0.5, 1.5, p.nnz_crs)
+        crow = np.repeat(np.arange(N), np.diff(p.crs_row_ptr))
+        dense_rows.append(crow)
+        dense_cols.append(np.asarray(p.crs_col))
+        vals.append(A.crs_val)
+        tail = np.bincount(crow, weights=A.crs_val, minlength=N)
+    else:
+        tail = np.zeros(N)
+    diag = -A.V.sum(axis=1) - tail + 0.5
+    A.V[np.arange(N), p.diag_slot] = diag
+    import scipy.sparse as sp
+    M = sp.csr_matrix((np.concatenate(vals), (np.concatenate(dense_rows), np.concatenate(dense_cols))),
+                      shape=(N, N))
+    M = M + sp.diags(diag)
+    return p, A, M
+
+
+@pytest.mark.parametrize("n,crs_tail", [(8, False), (20, False), (20, True), (5, True)])
+def test_bicgstab_batch_kernel_on_box_operators(n, crs_tail):
+    # the persistent BiCGStab kernels on 7-point rows (one block for small
+    # systems, the whole grid otherwise; CRS tail when rows overflow K):
+    # the 3-component batch against a direct solve, and each component
+    # against the single-vector solver (same arithmetic per component)
+    import scipy.sparse.linalg as spla
+    rng = np.random.default_rng(11 + n)
+    p, A, M = _box_operator(n, crs_tail, rng)
+    assert p.k == 7 and (p.nnz_crs > 0) == crs_tail
+    N = p.n
+    B = rng.normal(size=(N, 3))
+    cfg = SolveConfig(tolerance=1e-12, max_iters=2000)
+    X, reps = bicgstab_batched(A, B, np.zeros((N, 3)), cfg)
+    for c in range(3):
+        assert reps[c].converged, reps[c]
+        ref = spla.spsolve(M.tocsc(), B[:, c])
+        assert rel(X[:, c], ref) < 1e-9
+        x1, r1 = bicgstab(A, B[:, c], np.zeros(N), cfg)
+        assert abs(r1.iterations - reps[c].iterations) <= 1
+        assert rel(X[:, c], x1) < 1e-9
