@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s3[2] += ri * zi;
     }
   }
-  if (!team_reduce<3>(T, A.sync, A.partials, s3, red, rnd, sends)) {
+  if (!team_reduce<3, true>(T, A.sync, A.partials, s3, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       }
     }
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
-    if (!team_reduce<1>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<1, true>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     // next pass A's first index rows travel while this pass's reduction runs
     if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
     if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
-    if (!team_reduce<2>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<2, true>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
