@@ -6,6 +6,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "fvb_internal.cuh"
@@ -786,6 +787,57 @@ int fvb_upload_mesh(fvb_ctx* h, int64_t n_cells, int64_t n_faces, int64_t n_inte
                               smag, vol, w, d, db);
 }
 
+namespace fvb {
+// Stencil-code compression of the column indices (PatternView::code): the
+// solvers' SpMV passes read one byte per row instead of K int32 indices
+// when the rows' column-offset tuples (col - row per slot) fall into at
+// most kMaxCodes distinct patterns — every row of a structured hex mesh
+// does (27 tuples: interior, faces, edges, corners).  Rows outside the
+// dictionary are coded kEscapeCode and read their explicit indices; with
+// more than 1/16 of the rows escaping the codes are not used at all.  The
+// columns, and hence every product and sum, are exactly those of I.
+static int build_stencil_codes(Ctx* c, const std::vector<int>& Is, size_t nn, size_t kk) {
+  std::vector<uint8_t> code(nn, uint8_t(kEscapeCode));
+  std::vector<int> tab;
+  std::unordered_map<uint64_t, std::vector<int>> dict;  // hash -> codes
+  size_t escapes = 0;
+  std::vector<int> off(kk);
+  for (size_t i = 0; i < nn; ++i) {
+    uint64_t h = 1469598103934665603ull;
+    for (size_t s = 0; s < kk; ++s) {
+      const int col = Is[s * nn + i];
+      off[s] = col < 0 ? kPadOffset : col - int(i);
+      h = (h ^ uint32_t(off[s])) * 1099511628211ull;
+    }
+    int found = -1;
+    auto it = dict.find(h);
+    if (it != dict.end())
+      for (int q : it->second)
+        if (std::equal(off.begin(), off.end(), tab.begin() + size_t(q) * kk)) {
+          found = q;
+          break;
+        }
+    if (found < 0 && int(tab.size() / kk) < kMaxCodes) {
+      found = int(tab.size() / kk);
+      tab.insert(tab.end(), off.begin(), off.end());
+      dict[h].push_back(found);
+    }
+    if (found < 0) {
+      if (++escapes > nn / 16) return FVB_OK;  // not worth it: plain I
+    } else {
+      code[i] = uint8_t(found);
+    }
+  }
+  FVB_TRY(dalloc(c, &c->scode, nn));
+  FVB_CUDA(cudaMemcpy(c->scode, code.data(), nn, cudaMemcpyHostToDevice));
+  FVB_TRY(dalloc(c, &c->stab, tab.size()));
+  FVB_CUDA(cudaMemcpy(c->stab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
+  c->n_scode = int(tab.size() / kk);
+  c->n_sescape = int64_t(escapes);
+  return FVB_OK;
+}
+}  // namespace fvb
+
 int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
                        const int64_t* diag_slot, const int64_t* face_addr, int64_t n_face_pairs,
                        int64_t nnz_crs, const int64_t* crs_row_ptr, const int64_t* crs_col) {
@@ -859,6 +911,7 @@ int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
     return FVB_OK;
   };
   FVB_TRY(up(Is, &c->I));
+  if (kk <= 16) FVB_TRY(build_stencil_codes(c, Is, nn, kk));
   FVB_TRY(up(ds, &c->diag_slot));
   FVB_TRY(up(sf, &c->slot_face));
   if (nnz_crs) {
@@ -1405,6 +1458,13 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
   Ctx* c = &h->c;
   cudaSetDevice(c->dev);
   return run_step(c, cfg, u_speeds, rep, false);
+}
+
+int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape) {
+  Ctx* c = &h->c;
+  if (n_codes) *n_codes = c->scode ? c->n_scode : 0;
+  if (n_escape) *n_escape = c->scode ? c->n_sescape : 0;
+  return FVB_OK;
 }
 
 unsigned long long fvb_launch_count(void) { return g_launches.load(); }

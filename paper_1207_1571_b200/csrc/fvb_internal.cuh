@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <climits>
+
 #include <atomic>
 #include <string>
 #include <vector>
@@ -152,7 +154,17 @@ struct PatternView {
   const int* crs_ptr;    // [n+1] (nullptr when nnz_crs == 0)
   const int* crs_col;
   const int* crs_face;
+  // Stencil codes (nullptr when off): row i's column offsets are
+  // stab[code[i]*k + s] (col = i + offset; kPadOffset = padding, column 0),
+  // code kEscapeCode = read I.  Built at upload when few distinct offset
+  // tuples cover the rows (structured and block-structured meshes).
+  const uint8_t* code;
+  const int* stab;
+  int ncode;
 };
+constexpr int kMaxCodes = 255;      // distinct offset tuples per pattern
+constexpr int kEscapeCode = 255;    // row outside the dictionary: explicit I
+constexpr int kPadOffset = INT_MIN; // padding slot (column 0, value 0)
 
 struct BcView {
   const uint8_t* kind;   // [nb]
@@ -198,6 +210,10 @@ struct Ctx {
          *ky = nullptr, *kz = nullptr;
   // pattern
   int *I = nullptr, *diag_slot = nullptr, *slot_face = nullptr;
+  uint8_t* scode = nullptr;  // stencil codes (PatternView::code), or nullptr
+  int* stab = nullptr;
+  int n_scode = 0;
+  int64_t n_sescape = 0;     // rows coded kEscapeCode
   int *crs_ptr = nullptr, *crs_col = nullptr, *crs_face = nullptr;
   // boundary conditions: 0 = u (3 comps), 1 = p
   uint8_t* bc_kind[2] = {nullptr, nullptr};
@@ -239,7 +255,8 @@ struct Ctx {
                     cf_ptr, cf};
   }
   PatternView pattern() const {
-    return PatternView{nr, k, nnz_crs, I, diag_slot, slot_face, crs_ptr, crs_col, crs_face};
+    return PatternView{nr, k, nnz_crs, I, diag_slot, slot_face, crs_ptr, crs_col, crs_face,
+                       scode, stab, n_scode};
   }
   BcView bc(int field) const {
     return BcView{bc_kind[field], bc_patch[field], bc_fixed[field], bc_speed[field]};

@@ -135,6 +135,80 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
   return acc;
 }
 
+// Pass A over stencil-coded rows (PatternView::code): the ring carries
+// each row's one-byte code DEPTH rows ahead and the column offsets come
+// from the shared-memory copy of the code table; rows coded kEscapeCode
+// load their explicit indices.  Columns, products and order as
+// cg_pass_a_icols.
+template <int KT, int DEPTH>
+__device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const double* __restrict__ z,
+                                                  const double* __restrict__ po,
+                                                  double* __restrict__ pnew, double beta,
+                                                  bool first, int slot_new, int i, int end,
+                                                  int step, const int* __restrict__ s_tab) {
+  const PatternView& P = A.P;
+  const TeamView& T = A.T;
+  const int n = P.n;
+  const int* __restrict__ I = P.I;
+  const uint8_t* __restrict__ code = P.code;
+  const double* __restrict__ V = A.V;
+  const bool team = T.size > 1;
+  double acc = 0.0;
+  int cq[DEPTH];
+#pragma unroll
+  for (int d = 0; d < DEPTH; ++d) {
+    const int r = i + d * step;
+    cq[d] = r < end ? int(__ldcs(code + r)) : 0;
+  }
+  auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
+  while (i < end) {
+    double vi[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) vi[s] = __ldcs(V + size_t(s) * n + i);
+    const int cd = cq[0];
+#pragma unroll
+    for (int d = 0; d + 1 < DEPTH; ++d) cq[d] = cq[d + 1];
+    const int nx = i + DEPTH * step;
+    if (nx < end) cq[DEPTH - 1] = int(__ldcs(code + nx));
+    int ci[KT];
+    if (cd != kEscapeCode) {
+      const int* so = s_tab + cd * KT;
+#pragma unroll
+      for (int s = 0; s < KT; ++s) {
+        const int o = so[s];
+        ci[s] = o == kPadOffset ? 0 : i + o;
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) {
+        const int c = __ldcs(I + size_t(s) * n + i);
+        ci[s] = c < 0 ? 0 : c;
+      }
+    }
+    double pr[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * g(ci[s]);
+    double ev = pr[0];
+#pragma unroll
+    for (int s = 2; s < KT; s += 2) ev = ev + pr[s];
+    double y = ev;
+    if (KT > 1) {
+      double od = pr[1];
+#pragma unroll
+      for (int s = 3; s < KT; s += 2) od = od + pr[s];
+      y = ev + od;
+    }
+    const double qi = crs_tail(P, A.crs, i, y, g);
+    const double pi = g(i);
+    pnew[i] = pi;
+    A.q[i] = qi;
+    if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
+    acc += pi * qi;
+    i += step;
+  }
+  return acc;
+}
+
 template <int KT, bool STREAM>
 __device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double* __restrict__ z,
                                                  const double* __restrict__ po,
@@ -202,9 +276,16 @@ __device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double
 // gives every block one contiguous chunk swept in blockDim steps, so the
 // +-1 and +-n neighbours a row gathers were loaded by the same SM moments
 // earlier (L1 hits) and only the +-n^2 ones come from L2.
-template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0, int PB2 = 0>
+template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0, int PB2 = 0,
+          int SC = 0>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
+  // SC: stencil-coded pass A (PatternView::code) with the code table here
+  __shared__ int s_tab[SC ? kMaxCodes * (KT > 0 ? KT : 1) : 1];
+  if (SC) {
+    for (int j = threadIdx.x; j < A.P.ncode * KT; j += blockDim.x) s_tab[j] = A.P.stab[j];
+    __syncthreads();
+  }
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int nrows = P.n;
@@ -279,7 +360,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
-      if (PIPE >= 3 && KT > 0) {
+      if (SC && KT > 0) {
+        pq[0] = cg_pass_a_codes<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab);
+      } else if (PIPE >= 3 && KT > 0) {
         pq[0] = cg_pass_a_icols<KR, DR, (XB != 0)>(A, z, po, pnew, beta, first, slot_new, tid,
                                                    n, G, ring);
       } else if (PIPE && KT > 0) {
@@ -1299,7 +1382,12 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
     return e ? atoi(e) : -1;
   }();
   switch (c->k) {
-    case 5: FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;
+    case 5:
+      if (c->scode && variant != 20)
+        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1, 1>, prm, 1024, 1));
+      else
+        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1));
+      break;
     case 7:
       switch (variant) {
         case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;     // plain pass A
@@ -1307,7 +1395,15 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
         case 12: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;    // index ring, 2x512
         case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;  // + ring across barrier
         case 17: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;  // scalar pass B
-        default: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;
+        case 20: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;  // explicit I
+        default:
+          // stencil-coded rows when the pattern has codes (1 byte per row
+          // instead of K indices), else the explicit index ring
+          if (c->scode)
+            FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 1>, prm, 1024, 1));
+          else
+            FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1));
+          break;
       }
       break;
     default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;

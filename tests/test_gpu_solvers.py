@@ -205,3 +205,42 @@ def test_bicgstab_batch_kernel_on_box_operators(n, crs_tail):
         x1, r1 = bicgstab(A, B[:, c], np.zeros(N), cfg)
         assert abs(r1.iterations - reps[c].iterations) <= 1
         assert rel(X[:, c], x1) < 1e-9
+
+
+def test_stencil_codes_cg_bitwise_equals_explicit_indices():
+    # pass A on 1-byte stencil codes reads exactly the columns of the
+    # explicit index array: same iterates, bit for bit (FVB_CG_VARIANT=20
+    # forces the explicit-index kernel)
+    import json, os, subprocess, sys
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+    out = {}
+    for var in ("-1", "20"):
+        env = dict(os.environ, FVB_CG_VARIANT=var)
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "24", "60"],
+                             env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr
+        out[var] = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["-1"]["codes"] == 27 and out["20"]["codes"] == 0
+    assert out["-1"]["x_sha"] == out["20"]["x_sha"]
+    assert out["-1"]["res"] == out["20"]["res"]
+
+
+def test_stencil_code_dictionary():
+    import ctypes as C
+    from paper_1207_1571_b200 import _lib, cases
+    from paper_1207_1571_b200.device import context_for
+
+    def codes_of(pat):
+        ctx = context_for(None, None, pat)
+        nc, ne = C.c_int(), C.c_int64()
+        _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(nc), C.byref(ne)))
+        return nc.value, ne.value
+
+    box = cases.box_mesh(10, 9, 8, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
+    assert codes_of(sparse.build_pattern(box)) == (27, 0)
+    # a random renumbering leaves no common offset tuples: codes off
+    perm = np.random.default_rng(3).permutation(box.n_cells)
+    ni = box.n_internal
+    pairs = np.stack([perm[np.asarray(box.owner[:ni])], perm[np.asarray(box.neighbour)]], axis=1)
+    pairs = np.sort(pairs, axis=1)
+    assert codes_of(sparse.pattern_from_pairs(box.n_cells, pairs, 16)) == (0, 0)

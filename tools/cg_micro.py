@@ -2,7 +2,7 @@
 Laplacian-like SPD matrix (K = 7) through fvb_op_cg; prints device time per
 iteration and the algorithmic HBM rate (N(12K+96) bytes per iteration).
 Usage: python tools/cg_micro.py N ITERS  (FVB_CG_VARIANT selects the kernel)"""
-import ctypes as C, json, os, sys, time
+import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
 from paper_1207_1571_b200 import _lib, cases, sparse
@@ -29,10 +29,16 @@ for rpt in range(3):
     _lib.check(rc)
     res.append((rep.wall_time, rep.t_smvp, rep.t_daxpy, rep.t_reduction))
 t, ta, tb, tr = min(res)
-bytes_it = N * (12 * K + 96)
+codes, nesc = C.c_int(), C.c_int64()
+_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc)))
+# 1-byte stencil codes replace the K int32 indices when the pattern compresses
+use_codes = codes.value and os.environ.get("FVB_CG_VARIANT", "-1") == "-1"
+bytes_it = N * ((8 * K + 1 + 96) if use_codes else (12 * K + 96))
 setup_b = N * (12 * K + 80)
-print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "0"), "n": n, "iters": rep.iterations,
+print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "-1"), "n": n, "iters": rep.iterations,
                   "us_per_iter": 1e6 * t / iters,
                   "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
                   "us_reduce2x": 1e6 * tr / iters,
-                  "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1)}))
+                  "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1),
+                  "codes": codes.value if use_codes else 0, "res": rep.final_residual,
+                  "x_sha": hashlib.sha256(x.tobytes()).hexdigest()[:16]}))
