@@ -533,34 +533,55 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
 // column indices prefetched two rows ahead (the gather's address chain; see
 // cg_pass_a_icols) and evict-first matrix loads; body(i, y) consumes a row.
 // Same products and summation order as ell_rows_multi.
-template <int KT, int NC, typename Gt, typename Bt>
+// SC: stencil-coded rows (PatternView::code, table in shared memory s_tab):
+// the ring carries one code per row instead of KT indices.
+template <int KT, int NC, bool SC = false, typename Gt, typename Bt>
 __device__ __forceinline__ void spmv_sweep(const PatternView& P, const double* __restrict__ V,
                                            const double* crs, int i, int end, int step,
-                                           const bool* act, Gt gather, Bt body) {
+                                           const bool* act, Gt gather, Bt body,
+                                           const int* s_tab = nullptr) {
   const int n = P.n;
-  int c0[KT], c1[KT];
-  if (i < end) {
+  constexpr int KC = SC ? 1 : KT;  // ring entries per row
+  int c0[KC], c1[KC];
+  auto ring_load = [&](int (&cq)[KC], int r) {
+    if (SC) {
+      cq[0] = int(__ldcs(P.code + r));
+    } else {
 #pragma unroll
-    for (int s = 0; s < KT; ++s) c0[s] = __ldcs(P.I + size_t(s) * n + i);
-  }
-  if (i + step < end) {
-#pragma unroll
-    for (int s = 0; s < KT; ++s) c1[s] = __ldcs(P.I + size_t(s) * n + i + step);
-  }
+      for (int s = 0; s < KC; ++s) cq[s] = __ldcs(P.I + size_t(s) * n + r);
+    }
+  };
+  if (i < end) ring_load(c0, i);
+  if (i + step < end) ring_load(c1, i + step);
   while (i < end) {
     double v[KT];
     int ci[KT];
 #pragma unroll
-    for (int s = 0; s < KT; ++s) {
-      v[s] = __ldcs(V + size_t(s) * n + i);
-      ci[s] = c0[s] < 0 ? 0 : c0[s];
-      c0[s] = c1[s];
-    }
-    const int nx = i + 2 * step;
-    if (nx < end) {
+    for (int s = 0; s < KT; ++s) v[s] = __ldcs(V + size_t(s) * n + i);
+    if (SC) {
+      const int cd = c0[0];
+      if (cd != kEscapeCode) {
+        const int* so = s_tab + cd * KT;
 #pragma unroll
-      for (int s = 0; s < KT; ++s) c1[s] = __ldcs(P.I + size_t(s) * n + nx);
+        for (int s = 0; s < KT; ++s) {
+          const int o = so[s];
+          ci[s] = o == kPadOffset ? 0 : i + o;
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < KT; ++s) {
+          const int c = __ldcs(P.I + size_t(s) * n + i);
+          ci[s] = c < 0 ? 0 : c;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) ci[s] = c0[s] < 0 ? 0 : c0[s];
     }
+#pragma unroll
+    for (int s = 0; s < KC; ++s) c0[s] = c1[s];
+    const int nx = i + 2 * step;
+    if (nx < end) ring_load(c1, nx);
     double y[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -912,10 +933,16 @@ struct Bi3Params {
   double* result;
 };
 
-template <int KT, int NC>
+template <int KT, int NC, bool SC = false>
 __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A) {
   __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
   __shared__ CompState S[NC];
+  // SC: stencil-coded SpMV sweeps (PatternView::code) with the code table here
+  __shared__ int s_tab[SC ? kMaxCodes * (KT > 0 ? KT : 1) : 1];
+  if (SC) {
+    for (int j = threadIdx.x; j < A.P.ncode * KT; j += blockDim.x) s_tab[j] = A.P.stab[j];
+    __syncthreads();
+  }
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const RowRange R = team_rows(T, P.n);
@@ -1063,7 +1090,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       };
       if (KT > 0) {
-        spmv_sweep<KR, NC>(P, A.V, A.crs, tid, n, G, act, g, body);
+        spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
       } else {
         for (int i = tid; i < n; i += G) {
           double y[NC];
@@ -1110,7 +1137,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
 #pragma unroll
       for (int c = 0; c < NC; ++c) any_a = any_a || act[c];
       if (KT > 0 && any_a) {
-        spmv_sweep<KR, NC>(P, A.V, A.crs, tid, n, G, act, g, body);
+        spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
       } else {
         for (int i = tid; i < n; i += G) {
           double y[NC];
@@ -1499,9 +1526,18 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   prm.sync = c->sync;
   prm.partials = c->partials;
   prm.result = result;
+  static const int variant = [] {
+    const char* e = getenv("FVB_BI_VARIANT");
+    return e ? atoi(e) : -1;
+  }();
+  // stencil-coded SpMV sweeps when the pattern has codes (FVB_BI_VARIANT=20:
+  // explicit indices)
+  const bool sc = c->scode && variant != 20;
   switch (c->k) {
-    case 5: return coop_launch(c, k_bicgstab3<5, NC>, prm);
-    case 7: return coop_launch(c, k_bicgstab3<7, NC>, prm);
+    case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm)
+                      : coop_launch(c, k_bicgstab3<5, NC>, prm);
+    case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm)
+                      : coop_launch(c, k_bicgstab3<7, NC>, prm);
     default: return coop_launch(c, k_bicgstab3<0, NC>, prm);
   }
 }

@@ -152,10 +152,11 @@ def _box_operator(n, crs_tail, rng):
     pairs = np.stack([np.asarray(mesh.owner[:ni]), np.asarray(mesh.neighbour)], axis=1)
     N = mesh.n_cells
     if crs_tail:
-        # long-range couplings on ~2% of the rows with K capped at 7: the
-        # overflow entries go to the CRS tail
-        a = rng.choice(N, size=N // 50, replace=False)
-        b = (a + N // 3 + 7) % N
+        # random long-range couplings on ~2% of the rows with K capped at 7:
+        # the overflow entries go to the CRS tail and those rows escape the
+        # stencil codes
+        a = rng.choice(N, size=max(1, N // 50), replace=False)
+        b = rng.integers(0, N, size=a.size)
         extra = np.stack([np.minimum(a, b), np.maximum(a, b)], axis=1)
         pairs = np.unique(np.concatenate([pairs, extra[extra[:, 0] != extra[:, 1]]]), axis=0)
     p = sparse.pattern_from_pairs(N, pairs, 7)
@@ -207,20 +208,25 @@ def test_bicgstab_batch_kernel_on_box_operators(n, crs_tail):
         assert rel(X[:, c], x1) < 1e-9
 
 
-def test_stencil_codes_cg_bitwise_equals_explicit_indices():
+@pytest.mark.parametrize("mode", ["", "crs"])
+def test_stencil_codes_cg_bitwise_equals_explicit_indices(mode):
     # pass A on 1-byte stencil codes reads exactly the columns of the
     # explicit index array: same iterates, bit for bit (FVB_CG_VARIANT=20
-    # forces the explicit-index kernel)
+    # forces the explicit-index kernel); "crs": escaped rows + CRS tail
     import json, os, subprocess, sys
     root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
     out = {}
     for var in ("-1", "20"):
         env = dict(os.environ, FVB_CG_VARIANT=var)
-        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "24", "60"],
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "24", "60", mode],
                              env=env, capture_output=True, text=True, timeout=600)
         assert res.returncode == 0, res.stderr
         out[var] = json.loads(res.stdout.strip().splitlines()[-1])
-    assert out["-1"]["codes"] == 27 and out["20"]["codes"] == 0
+    if mode:
+        assert out["-1"]["escaped"] > 0 and out["-1"]["nnz_crs"] > 0
+    else:
+        assert out["-1"]["codes"] == 27 and out["-1"]["escaped"] == 0
+    assert out["20"]["codes"] == 0
     assert out["-1"]["x_sha"] == out["20"]["x_sha"]
     assert out["-1"]["res"] == out["20"]["res"]
 
@@ -244,3 +250,22 @@ def test_stencil_code_dictionary():
     pairs = np.stack([perm[np.asarray(box.owner[:ni])], perm[np.asarray(box.neighbour)]], axis=1)
     pairs = np.sort(pairs, axis=1)
     assert codes_of(sparse.pattern_from_pairs(box.n_cells, pairs, 16)) == (0, 0)
+
+
+@pytest.mark.parametrize("mode", ["", "crs"])
+def test_stencil_codes_bicgstab_bitwise_equals_explicit_indices(mode):
+    # batched BiCGStab SpMV sweeps on stencil codes (FVB_BI_VARIANT=20 forces
+    # the explicit indices); "crs" adds rows that overflow K (escaped rows
+    # and a CRS tail)
+    import json, os, subprocess, sys
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+    out = {}
+    for var in ("-1", "20"):
+        env = dict(os.environ, FVB_BI_VARIANT=var)
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "bi_micro.py"), "20", "30", mode],
+                             env=env, capture_output=True, text=True, timeout=600)
+        assert res.returncode == 0, res.stderr
+        out[var] = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["-1"]["codes"] > 0 and out["20"]["codes"] == 0
+    assert out["-1"]["x_sha"] == out["20"]["x_sha"]
+    assert out["-1"]["iters"] == out["20"]["iters"] and out["-1"]["res"] == out["20"]["res"]

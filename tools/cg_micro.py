@@ -1,7 +1,8 @@
 """CG kernel microbenchmark: fixed-iteration Jacobi-PCG on a cavity
 Laplacian-like SPD matrix (K = 7) through fvb_op_cg; prints device time per
 iteration and the algorithmic HBM rate (N(12K+96) bytes per iteration).
-Usage: python tools/cg_micro.py N ITERS  (FVB_CG_VARIANT selects the kernel)"""
+Usage: python tools/cg_micro.py N ITERS [crs]  (FVB_CG_VARIANT selects the kernel; "crs"
+adds long-range couplings: CRS tail + escaped stencil-code rows)"""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
@@ -11,16 +12,29 @@ from paper_1207_1571_b200.device import context_for
 n = int(sys.argv[1]); iters = int(sys.argv[2])
 t0 = time.time()
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
-pat = sparse.build_pattern(mesh)
+if len(sys.argv) > 3 and sys.argv[3] == "crs":
+    # symmetric long-range couplings on ~2% of the rows with K capped at 7:
+    # overflow entries go to the CRS tail, those rows escape the stencil codes
+    ni = mesh.n_internal
+    pairs = np.stack([np.asarray(mesh.owner[:ni]), np.asarray(mesh.neighbour)], axis=1)
+    rng = np.random.default_rng(1)
+    a = rng.choice(mesh.n_cells, size=max(1, mesh.n_cells // 50), replace=False)
+    bb = rng.integers(0, mesh.n_cells, size=a.size)  # random partners: distinct offset tuples
+    extra = np.stack([np.minimum(a, bb), np.maximum(a, bb)], axis=1)
+    pairs = np.unique(np.concatenate([pairs, extra[extra[:, 0] != extra[:, 1]]]), axis=0)
+    pat = sparse.pattern_from_pairs(mesh.n_cells, pairs, 7)
+else:
+    pat = sparse.build_pattern(mesh)
 N, K = pat.n, pat.k
 V = np.where(pat.I >= 0, -1.0, 0.0)
-V[np.arange(N), pat.diag_slot] = (pat.I >= 0).sum(axis=1) - 1 + 0.01
+ncrs = np.diff(pat.crs_row_ptr) if pat.nnz_crs else np.zeros(N, dtype=np.int64)
+V[np.arange(N), pat.diag_slot] = (pat.I >= 0).sum(axis=1) - 1 + ncrs + 0.01
 b = np.random.default_rng(0).normal(size=N)
 x = np.empty(N)
 ctx = context_for(None, None, pat)
 rep = _lib.SolveReportC()
 P = _lib.ptr
-crs = np.zeros(max(pat.nnz_crs, 1))
+crs = np.full(max(pat.nnz_crs, 1), -1.0)
 setup = time.time() - t0
 res = []
 for rpt in range(3):
@@ -40,5 +54,6 @@ print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "-1"), "n": n, "it
                   "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
                   "us_reduce2x": 1e6 * tr / iters,
                   "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1),
-                  "codes": codes.value if use_codes else 0, "res": rep.final_residual,
+                  "codes": codes.value if use_codes else 0, "escaped": nesc.value if use_codes else 0,
+                  "nnz_crs": int(pat.nnz_crs), "res": rep.final_residual,
                   "x_sha": hashlib.sha256(x.tobytes()).hexdigest()[:16]}))
