@@ -607,6 +607,9 @@ def run_ours(args):
                      "bytes_per_step": step_bytes / args.steps},
         "iterations_per_step": {"cg": sum(cg_iters) / args.steps,
                                 "bicgstab": sum(bi_iters) / args.steps},
+        "cg_iterations_per_launch": [it for it, _ in cg_k],
+        "bicgstab_iterations_per_launch": (lambda b: [max(b[i:i + 3]) for i in range(0, len(b), 3)])(
+            [it for sv, it, _ in kernel_rows if sv == "bicgstab"]),
         "kernel_ms_per_step": {
             "k_cg": 1e3 * D.max(sum(ks for sv, _, ks in kernel_rows if sv == "cg")) / args.steps,
             # the 3 batched momentum solves share one launch (its time is on each row)
