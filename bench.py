@@ -20,9 +20,10 @@ One JSON line on rank 0:
                every step uploads u, p, flux from pinned memory and
                downloads them again (bytes counted per step, all ranks)
   roofline     dominant kernel = persistent Jacobi-PCG (k_cg): algorithmic
-               bytes N(12K+80) + iters * N(8K+idx+96) per launch (SURVEY.md
+               bytes N(12K+80) + iters * N(8K+idx+vec) per launch (SURVEY.md
                §8(d); idx = 4K bytes of int32 column indices per row, or 1
-               byte of stencil code when the pattern compresses) over its
+               byte of stencil code when the pattern compresses; vec = 96,
+               or 88 when x += alpha p rides in the next pass A) over its
                CUDA-event duration; peak = MEASURED_PEAKS
                hbm_gbs x N GPUs; traffic = ncu DRAM bytes per launch scaled
                from profiles/ncu_k_cg_traffic.json
@@ -338,16 +339,18 @@ class _Dist:
 
 def index_bytes_per_row(h, n_rows, K):
     """Column-index bytes pass A reads per row: 4K (int32 ELL indices), or
-    1 byte of stencil code plus 4K for each escaped row (fvb_pattern_codes)."""
+    1 byte of stencil code plus 4K for each escaped row; and whether CG
+    folds x += alpha p into pass A (then pass B does not re-read p: 88
+    instead of 96 vector bytes per row) (fvb_pattern_codes)."""
     import ctypes as C
 
     from paper_1207_1571_b200 import _lib
 
-    nc, ne = C.c_int(), C.c_int64()
-    _lib.check(_lib.lib.fvb_pattern_codes(h, C.byref(nc), C.byref(ne)))
+    nc, ne, df = C.c_int(), C.c_int64(), C.c_int()
+    _lib.check(_lib.lib.fvb_pattern_codes(h, C.byref(nc), C.byref(ne), C.byref(df)))
     if nc.value == 0:
-        return 4.0 * K, 0
-    return 1.0 + 4.0 * K * ne.value / max(n_rows, 1), nc.value
+        return 4.0 * K, 0, df.value
+    return 1.0 + 4.0 * K * ne.value / max(n_rows, 1), nc.value, df.value
 
 
 def measure_c2(steps, warmup):
@@ -374,8 +377,9 @@ def measure_c2(steps, warmup):
     _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
     N, K = case.mesh.n_cells, st.pattern.k
     cg = [(it, ks) for sv, it, ks in rows if sv == "cg"]
-    idx_row, _ = index_bytes_per_row(h, N, K)
-    cg_bytes = sum(N * (12 * K + 80) + it * N * (8 * K + idx_row + 96) for it, _ in cg)
+    idx_row, _, defer = index_bytes_per_row(h, N, K)
+    cg_bytes = sum(N * (12 * K + 80) + it * N * (8 * K + idx_row + (88 if defer else 96))
+                   for it, _ in cg)
     cg_time = sum(ks for _, ks in cg)
     peak, _ = peaks()
     ms_step = ms.value / steps
@@ -491,8 +495,9 @@ def run_ours(args):
     # dominant kernel: persistent PCG (k_cg), bytes of this rank's rows
     cg_k = [(it, ks) for (solver, it, ks) in kernel_rows if solver == "cg"]
     b_setup = n_local * (12 * K + 80)
-    idx_row, n_codes = index_bytes_per_row(h, n_local, K)
-    b_iter = n_local * (8 * K + idx_row + 96)
+    idx_row, n_codes, defer = index_bytes_per_row(h, n_local, K)
+    vec_row = 88 if defer else 96
+    b_iter = n_local * (8 * K + idx_row + vec_row)
     cg_bytes = D.sum(sum(b_setup + it * b_iter for it, _ in cg_k))
     cg_time = D.max(sum(ks for _, ks in cg_k))
     peak1, peak_kind = peaks()
@@ -598,10 +603,12 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_cg (persistent Jacobi-PCG)", "peak_kind": peak_kind,
-                     "bytes_model": (f"N*(12K+80) + iters*N*(8K+{idx_row:.3g}+96), K={K}; "
+                     "bytes_model": (f"N*(12K+80) + iters*N*(8K+{idx_row:.3g}+{vec_row}), K={K}; "
                                      + (f"column indices as 1-byte stencil codes ({n_codes} "
                                         "offset tuples) + explicit indices of escaped rows"
-                                        if n_codes else "explicit int32 column indices")),
+                                        if n_codes else "explicit int32 column indices")
+                                     + ("; x += alpha p folded into the next SpMV pass"
+                                        if defer else "")),
                      "launches": len(cg_k), "mean_iters": mean_iters},
         "step_hbm": {"achieved_gbs": step_gbs, "frac": step_gbs / peak,
                      "bytes_per_step": step_bytes / args.steps},

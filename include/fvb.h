@@ -324,11 +324,13 @@ int fvb_team_allreduce(fvb_ctx* ctx, double* vals, int m, int op);
  * of the SMs so every rank's solver kernel is co-resident */
 int fvb_set_sm_share(fvb_ctx* ctx, int share);
 
-/* stencil-code compression of the uploaded pattern (no reference
- * counterpart; bench/roofline evidence): n_codes distinct column-offset
- * tuples (0 = off, the solvers read the explicit indices), n_escape rows
- * outside the dictionary */
-int fvb_pattern_codes(fvb_ctx* ctx, int* n_codes, int64_t* n_escape);
+/* solver data formats of the uploaded pattern (no reference counterpart;
+ * bench/roofline evidence): n_codes distinct column-offset tuples of the
+ * stencil-code compression (0 = off, the solvers read the explicit
+ * indices), n_escape rows outside the dictionary, cg_defer_x = 1 when CG
+ * folds x += alpha p into the next SpMV pass.  Any pointer
+ * may be NULL. */
+int fvb_pattern_codes(fvb_ctx* ctx, int* n_codes, int64_t* n_escape, int* cg_defer_x);
 
 /* number of kernels libfvb has launched in this process (bench evidence) */
 unsigned long long fvb_launch_count(void);

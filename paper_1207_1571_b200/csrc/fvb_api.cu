@@ -1460,10 +1460,11 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
   return run_step(c, cfg, u_speeds, rep, false);
 }
 
-int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape) {
+int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape, int* cg_defer_x) {
   Ctx* c = &h->c;
   if (n_codes) *n_codes = c->scode ? c->n_scode : 0;
   if (n_escape) *n_escape = c->scode ? c->n_sescape : 0;
+  if (cg_defer_x) *cg_defer_x = cg_defers_x(c) ? 1 : 0;
   return FVB_OK;
 }
 

@@ -682,6 +682,9 @@ enum SolveErr {
 // x must hold x0 on entry (ghost entries current); returns solution in x.
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol,
              double abs_tol, int max_iters, SolveOut* out);
+// true when cg_solve folds x += alpha p into the next pass A (default
+// kernel, 7-point rows)
+bool cg_defers_x(const Ctx* c);
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
                    double* const* x, double tol, double abs_tol, int max_iters,
                    SolveOut* out);

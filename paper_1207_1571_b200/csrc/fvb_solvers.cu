@@ -83,7 +83,9 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
                                                   bool first, int slot_new, int i, int end,
-                                                  int step, int (&cq)[DEPTH][KT]) {
+                                                  int step, int (&cq)[DEPTH][KT],
+                                                  double* __restrict__ xd = nullptr,
+                                                  double alpha_prev = 0.0) {
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int n = P.n;
@@ -130,6 +132,8 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
     A.q[i] = qi;
     if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
     acc += pi * qi;
+    // deferred x += alpha p of the previous iteration (po is that p)
+    if (xd && !first) xd[i] = __ldcs(xd + i) + alpha_prev * po[i];
     i += step;
   }
   return acc;
@@ -145,7 +149,8 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
                                                   bool first, int slot_new, int i, int end,
-                                                  int step, const int* __restrict__ s_tab) {
+                                                  int step, const int* __restrict__ s_tab,
+                                                  double* __restrict__ xd, double alpha_prev) {
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int n = P.n;
@@ -204,6 +209,8 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
     A.q[i] = qi;
     if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
     acc += pi * qi;
+    // deferred x += alpha p of the previous iteration (po is that p)
+    if (xd && !first) xd[i] = __ldcs(xd + i) + alpha_prev * po[i];
     i += step;
   }
   return acc;
@@ -277,7 +284,7 @@ __device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double
 // +-1 and +-n neighbours a row gathers were loaded by the same SM moments
 // earlier (L1 hits) and only the +-n^2 ones come from L2.
 template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0, int PB2 = 0,
-          int SC = 0>
+          int SC = 0, int DF = 0>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
   // SC: stencil-coded pass A (PatternView::code) with the code table here
@@ -350,6 +357,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
   constexpr int KR = KT > 0 ? KT : 1;
   constexpr int DR = PIPE >= 4 ? PIPE - 2 : 1;
+  // DEFER (DF): x += alpha p of iteration k runs in pass A of iteration
+  // k + 1 (which holds that p as its old p), or in a final sweep — pass B
+  // then streams r, q, 1/D and z only; same expression x + alpha p per row
+  constexpr bool DEFER = DF && (SC != 0 || PIPE >= 3) && KT > 0;
+  double alpha_prev = 0.0;
+  const double* p_pend = nullptr;  // p whose x update is still pending
   int ring[DR][KR];
   if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
   while (!conv && it < A.max_iters) {
@@ -361,10 +374,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
       if (SC && KT > 0) {
-        pq[0] = cg_pass_a_codes<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab);
+        pq[0] = cg_pass_a_codes<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab,
+                                        DEFER ? A.x : nullptr, alpha_prev);
       } else if (PIPE >= 3 && KT > 0) {
         pq[0] = cg_pass_a_icols<KR, DR, (XB != 0)>(A, z, po, pnew, beta, first, slot_new, tid,
-                                                   n, G, ring);
+                                                   n, G, ring, DEFER ? A.x : nullptr, alpha_prev);
       } else if (PIPE && KT > 0) {
         pq[0] = cg_pass_a_pipe<(KT > 0 ? KT : 1), (PIPE > 1)>(A, z, po, pnew, beta, first,
                                                                 slot_new, tid, n, G);
@@ -380,12 +394,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
         }
       }
     }
+    if (DEFER) p_pend = nullptr;  // pass A applied the previous update
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
     if (!team_reduce<1, true>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
-    // pass B: x += alpha p, r -= alpha q, z = r / D, ||r||^2, r.z
+    // pass B: x += alpha p (DEFER: in the next pass A, or the final sweep),
+    // r -= alpha q, z = r / D, ||r||^2, r.z
     double s2[2] = {0.0, 0.0};
     int i_scalar = tid;
     if (PB2 && !CONTIG && vec_ok) {
@@ -393,19 +409,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       const int npair = n >> 1;
       for (int j = tid; j < npair; j += G) {
         const int i = 2 * j;
-        const double2 pv = __ldcg(reinterpret_cast<const double2*>(pnew + i));
-        const double2 xv = __ldcg(reinterpret_cast<const double2*>(A.x + i));
+        if (!DEFER) {
+          const double2 pv = __ldcg(reinterpret_cast<const double2*>(pnew + i));
+          const double2 xv = __ldcg(reinterpret_cast<const double2*>(A.x + i));
+          double2 xo;
+          xo.x = xv.x + alpha * pv.x;
+          xo.y = xv.y + alpha * pv.y;
+          *reinterpret_cast<double2*>(A.x + i) = xo;
+        }
         const double2 rv = __ldcg(reinterpret_cast<const double2*>(A.r + i));
         const double2 qv = __ldcg(reinterpret_cast<const double2*>(A.q + i));
         const double2 iv = __ldcg(reinterpret_cast<const double2*>(inv + i));
-        double2 xo, ro, zo;
-        xo.x = xv.x + alpha * pv.x;
-        xo.y = xv.y + alpha * pv.y;
+        double2 ro, zo;
         ro.x = rv.x - alpha * qv.x;
         ro.y = rv.y - alpha * qv.y;
         zo.x = ro.x * iv.x;
         zo.y = ro.y * iv.y;
-        *reinterpret_cast<double2*>(A.x + i) = xo;
         *reinterpret_cast<double2*>(A.r + i) = ro;
         *reinterpret_cast<double2*>(A.z + i) = zo;
         if (team && i + 1 >= T.n_inner) {
@@ -420,8 +439,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       i_scalar = 2 * npair + tid;  // odd tail row
     }
     for (int i = i_scalar; i < n; i += G) {
-      const double pi = pnew[i];
-      A.x[i] = A.x[i] + alpha * pi;
+      if (!DEFER) A.x[i] = A.x[i] + alpha * pnew[i];
       const double ri = A.r[i] - alpha * A.q[i];
       const double zi = ri * inv[i];
       A.r[i] = ri;
@@ -433,6 +451,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     // next pass A's first index rows travel while this pass's reduction runs
     if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
     if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
+    if (DEFER) {
+      p_pend = pnew;
+      alpha_prev = alpha;
+    }
     if (!team_reduce<2, true>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
@@ -443,6 +465,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     double* t = pold; pold = pnew; pnew = t;
     slot_new = (slot_new == A.slot_pb) ? A.slot_pa : A.slot_pb;
     first = false;
+  }
+  if (DEFER && p_pend && err != SE_TIMEOUT) {
+    // the last iteration's x += alpha p (own rows only: no barrier needed)
+    for (int i = tid; i < n; i += G) A.x[i] = A.x[i] + alpha_prev * p_pend[i];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     A.result[0] = it;
@@ -1377,6 +1403,21 @@ std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row
 
 // Work vectors are pool slots S_SCR.. (so the ghost entries can be written
 // by the neighbour ranks).
+static int cg_variant() {
+  static const int v = [] {
+    const char* e = getenv("FVB_CG_VARIANT");
+    return e ? atoi(e) : -1;
+  }();
+  return v;
+}
+
+// x += alpha p folded into the next pass A: 426.6 -> 398.4 us per
+// iteration at 16.8M rows, even at 2.1M (57.3 vs 56.9 us, one call;
+// profiles/r01_cg_variants.md)
+bool cg_defers_x(const Ctx* c) {
+  return c->k == 7 && (cg_variant() == 22 || cg_variant() == -1);
+}
+
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double abs_tol,
              int max_iters, SolveOut* out) {
   double* inv = c->slot(S_SCR + 0);
@@ -1404,10 +1445,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   // address chain), evict-first matrix loads, grid-strided rows, one
   // 1024-thread block per SM, pass B on row pairs with 16-byte L2-only
   // loads (profiles/r01_cg_variants.md).
-  static const int variant = [] {
-    const char* e = getenv("FVB_CG_VARIANT");
-    return e ? atoi(e) : -1;
-  }();
+  const int variant = cg_variant();
   switch (c->k) {
     case 5:
       if (c->scode && variant != 20)
@@ -1416,6 +1454,14 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
         FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1));
       break;
     case 7:
+      if (cg_defers_x(c)) {
+        // x update folded into pass A (profiles/r01_cg_variants.md)
+        if (c->scode)
+          FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 1, 1>, prm, 1024, 1));
+        else
+          FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 0, 1>, prm, 1024, 1));
+        break;
+      }
       switch (variant) {
         case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;     // plain pass A
         case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;     // pipelined I/V
@@ -1423,6 +1469,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
         case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;  // + ring across barrier
         case 17: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;  // scalar pass B
         case 20: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;  // explicit I
+        case 22: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 1, 1>, prm, 1024, 1)); break;  // codes + deferred x
         default:
           // stencil-coded rows when the pattern has codes (1 byte per row
           // instead of K indices), else the explicit index ring

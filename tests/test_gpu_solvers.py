@@ -216,7 +216,7 @@ def test_stencil_codes_cg_bitwise_equals_explicit_indices(mode):
     import json, os, subprocess, sys
     root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
     out = {}
-    for var in ("-1", "20"):
+    for var in ("-1", "20", "22"):  # 22: codes + x update deferred into pass A
         env = dict(os.environ, FVB_CG_VARIANT=var)
         res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "24", "60", mode],
                              env=env, capture_output=True, text=True, timeout=600)
@@ -227,8 +227,9 @@ def test_stencil_codes_cg_bitwise_equals_explicit_indices(mode):
     else:
         assert out["-1"]["codes"] == 27 and out["-1"]["escaped"] == 0
     assert out["20"]["codes"] == 0
-    assert out["-1"]["x_sha"] == out["20"]["x_sha"]
-    assert out["-1"]["res"] == out["20"]["res"]
+    for var in ("-1", "22"):
+        assert out[var]["x_sha"] == out["20"]["x_sha"]
+        assert out[var]["res"] == out["20"]["res"]
 
 
 def test_stencil_code_dictionary():
@@ -239,7 +240,7 @@ def test_stencil_code_dictionary():
     def codes_of(pat):
         ctx = context_for(None, None, pat)
         nc, ne = C.c_int(), C.c_int64()
-        _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(nc), C.byref(ne)))
+        _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(nc), C.byref(ne), None))
         return nc.value, ne.value
 
     box = cases.box_mesh(10, 9, 8, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])

@@ -43,17 +43,18 @@ for rpt in range(3):
     _lib.check(rc)
     res.append((rep.wall_time, rep.t_smvp, rep.t_daxpy, rep.t_reduction))
 t, ta, tb, tr = min(res)
-codes, nesc = C.c_int(), C.c_int64()
-_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc)))
+codes, nesc, defer = C.c_int(), C.c_int64(), C.c_int()
+_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer)))
 # 1-byte stencil codes replace the K int32 indices when the pattern compresses
-use_codes = codes.value and os.environ.get("FVB_CG_VARIANT", "-1") == "-1"
-bytes_it = N * ((8 * K + 1 + 96) if use_codes else (12 * K + 96))
+use_codes = codes.value and os.environ.get("FVB_CG_VARIANT", "-1") in ("-1", "22")
+# deferred x update (large systems): pass B no longer re-reads p
+bytes_it = N * ((8 * K + 1 if use_codes else 12 * K) + (88 if defer.value else 96))
 setup_b = N * (12 * K + 80)
 print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "-1"), "n": n, "iters": rep.iterations,
                   "us_per_iter": 1e6 * t / iters,
                   "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
                   "us_reduce2x": 1e6 * tr / iters,
                   "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1),
-                  "codes": codes.value if use_codes else 0, "escaped": nesc.value if use_codes else 0,
+                  "codes": codes.value if use_codes else 0, "defer_x": defer.value, "escaped": nesc.value if use_codes else 0,
                   "nnz_crs": int(pat.nnz_crs), "res": rep.final_residual,
                   "x_sha": hashlib.sha256(x.tobytes()).hexdigest()[:16]}))

@@ -30,12 +30,13 @@ def main(raw, log, kind, idx, out):
     line = [l for l in open(log) if l.startswith('{"metric"')][-1]
     b = json.loads(line)
     N, K = b["config"]["cells"], b["config"]["K"]
-    m = re.search(r"iters\*N\*\(8K\+([0-9.]+)\+96\)", b["roofline"]["bytes_model"])
+    m = re.search(r"iters\*N\*\(8K\+([0-9.]+)\+([0-9]+)\)", b["roofline"]["bytes_model"])
     idx_row = float(m.group(1)) if m else 4.0 * K
+    vec_row = float(m.group(2)) if m else 96.0
     if kind == "cg":
         it = b["cg_iterations_per_launch"][idx]
-        alg = N * (12 * K + 80) + it * N * (8 * K + idx_row + 96)
-        model = f"N(12K+80) + iters N(8K+{idx_row:g}+96)"
+        alg = N * (12 * K + 80) + it * N * (8 * K + idx_row + vec_row)
+        model = f"N(12K+80) + iters N(8K+{idx_row:g}+{vec_row:g})"
     else:
         it = b["bicgstab_iterations_per_launch"][idx]
         per_row = 600.0 - (2 * (4 * K - idx_row))
