@@ -347,7 +347,7 @@ def index_bytes_per_row(h, n_rows, K):
     from paper_1207_1571_b200 import _lib
 
     nc, ne, df = C.c_int(), C.c_int64(), C.c_int()
-    _lib.check(_lib.lib.fvb_pattern_codes(h, C.byref(nc), C.byref(ne), C.byref(df)))
+    _lib.check(_lib.lib.fvb_pattern_codes(h, C.byref(nc), C.byref(ne), C.byref(df), None))
     if nc.value == 0:
         return 4.0 * K, 0, df.value
     return 1.0 + 4.0 * K * ne.value / max(n_rows, 1), nc.value, df.value

@@ -187,7 +187,8 @@ _sig("fvb_state_apply_bcs", I, vp, dp)
 _sig("fvb_op_face_flux", I, vp, dp, dp, dp)
 _sig("fvb_continuity_error", I, vp, dp)
 _sig("fvb_sync", I, vp)
-_sig("fvb_pattern_codes", I, vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int))
+_sig("fvb_pattern_codes", I, vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int),
+     C.POINTER(C.c_int64))
 _sig("fvb_launch_count", C.c_ulonglong)
 _sig("fvb_host_register", I, vp, I64)
 _sig("fvb_host_unregister", I, vp)

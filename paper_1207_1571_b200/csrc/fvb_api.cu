@@ -838,6 +838,71 @@ static int build_stencil_codes(Ctx* c, const std::vector<int>& Is, size_t nn, si
 }
 }  // namespace fvb
 
+namespace fvb {
+// Reverse Cuthill-McKee order of the pattern's row graph (CG on meshes whose
+// numbering leaves no stencil codes, e.g. a randomly renumbered mesh): BFS
+// from a minimum-degree row of every component, neighbours by ascending
+// degree, reversed.  Only the solver's internal order changes: every row
+// keeps its slots in the same order (same products, same sums); only the
+// grouping of the dot products over rows moves.
+static int build_rcm(Ctx* c, const std::vector<int>& Is, const std::vector<int>& ds, size_t nn,
+                     size_t kk) {
+  std::vector<int> deg(nn, 0);
+  for (size_t i = 0; i < nn; ++i)
+    for (size_t s = 0; s < kk; ++s) {
+      const int col = Is[s * nn + i];
+      if (col >= 0 && size_t(col) != i) deg[i]++;
+    }
+  std::vector<int> order;
+  order.reserve(nn);
+  std::vector<char> seen(nn, 0);
+  std::vector<int> by_deg(nn);
+  for (size_t i = 0; i < nn; ++i) by_deg[i] = int(i);
+  std::stable_sort(by_deg.begin(), by_deg.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+  std::vector<int> nb;
+  for (int start : by_deg) {
+    if (seen[start]) continue;
+    seen[start] = 1;
+    size_t head = order.size();
+    order.push_back(start);
+    while (head < order.size()) {
+      const int i = order[head++];
+      nb.clear();
+      for (size_t s = 0; s < kk; ++s) {
+        const int col = Is[s * nn + size_t(i)];
+        if (col >= 0 && col != i && !seen[col]) {
+          seen[col] = 1;
+          nb.push_back(col);
+        }
+      }
+      std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+      order.insert(order.end(), nb.begin(), nb.end());
+    }
+  }
+  std::reverse(order.begin(), order.end());  // perm[new] = old
+  std::vector<int> iperm(nn);
+  for (size_t r = 0; r < nn; ++r) iperm[size_t(order[r])] = int(r);
+  std::vector<int> Ip(nn * kk), dsp(nn);
+  for (size_t r = 0; r < nn; ++r) {
+    const size_t o = size_t(order[r]);
+    dsp[r] = ds[o];
+    for (size_t s = 0; s < kk; ++s) {
+      const int col = Is[s * nn + o];
+      Ip[s * nn + r] = col < 0 ? -1 : iperm[size_t(col)];
+    }
+  }
+  auto up = [&](const std::vector<int>& v, int** o) -> int {
+    FVB_TRY(dalloc(c, o, v.size()));
+    FVB_CUDA(cudaMemcpy(*o, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    return FVB_OK;
+  };
+  FVB_TRY(up(order, &c->rcm_perm));
+  FVB_TRY(up(Ip, &c->rcm_I));
+  FVB_TRY(up(dsp, &c->rcm_ds));
+  return FVB_OK;
+}
+}  // namespace fvb
+
 int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
                        const int64_t* diag_slot, const int64_t* face_addr, int64_t n_face_pairs,
                        int64_t nnz_crs, const int64_t* crs_row_ptr, const int64_t* crs_col) {
@@ -912,6 +977,10 @@ int fvb_upload_pattern(fvb_ctx* h, int64_t n, int64_t k, const int64_t* I,
   };
   FVB_TRY(up(Is, &c->I));
   if (kk <= 16) FVB_TRY(build_stencil_codes(c, Is, nn, kk));
+  // no stencil codes on a large single-domain 7-point pattern without CRS
+  // tail: CG runs in RCM order (cg_solve)
+  if (!c->scode && kk == 7 && nnz_crs == 0 && c->nc == c->nr && nn >= 65536)
+    FVB_TRY(build_rcm(c, Is, ds, nn, kk));
   FVB_TRY(up(ds, &c->diag_slot));
   FVB_TRY(up(sf, &c->slot_face));
   if (nnz_crs) {
@@ -1460,11 +1529,13 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
   return run_step(c, cfg, u_speeds, rep, false);
 }
 
-int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape, int* cg_defer_x) {
+int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape, int* cg_defer_x,
+                      int64_t* cg_rcm_solves) {
   Ctx* c = &h->c;
   if (n_codes) *n_codes = c->scode ? c->n_scode : 0;
   if (n_escape) *n_escape = c->scode ? c->n_sescape : 0;
   if (cg_defer_x) *cg_defer_x = cg_defers_x(c) ? 1 : 0;
+  if (cg_rcm_solves) *cg_rcm_solves = c->cg_rcm_solves;
   return FVB_OK;
 }
 

@@ -214,6 +214,14 @@ struct Ctx {
   int* stab = nullptr;
   int n_scode = 0;
   int64_t n_sescape = 0;     // rows coded kEscapeCode
+  // bandwidth-reducing (reverse Cuthill-McKee) order for CG on patterns
+  // without stencil codes: rcm_perm[new] = old row, permuted slot-major
+  // columns and diagonal slots; the per-solve permuted matrix in rcm_V
+  int* rcm_perm = nullptr;
+  int* rcm_I = nullptr;
+  int* rcm_ds = nullptr;
+  double* rcm_V = nullptr;
+  int64_t cg_rcm_solves = 0;
   int *crs_ptr = nullptr, *crs_col = nullptr, *crs_face = nullptr;
   // boundary conditions: 0 = u (3 comps), 1 = p
   uint8_t* bc_kind[2] = {nullptr, nullptr};

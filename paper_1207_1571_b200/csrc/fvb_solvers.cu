@@ -1403,6 +1403,29 @@ std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row
 
 // Work vectors are pool slots S_SCR.. (so the ghost entries can be written
 // by the neighbour ranks).
+// RCM-ordered CG (Ctx::rcm_*): gather the system into the permuted order
+// (matrix slots, b, x0, 1/D), and scatter x back after the solve.
+template <int KT>
+__global__ void k_rcm_gather(int n, const int* __restrict__ perm, const double* __restrict__ V,
+                             const double* __restrict__ b, const double* __restrict__ x,
+                             const double* __restrict__ inv, double* __restrict__ Vp,
+                             double* __restrict__ bp, double* __restrict__ xp,
+                             double* __restrict__ invp) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int o = perm[r];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) Vp[size_t(s) * n + r] = V[size_t(s) * n + o];
+    bp[r] = b[o];
+    xp[r] = x[o];
+    invp[r] = inv[o];
+  }
+}
+__global__ void k_rcm_scatter(int n, const int* __restrict__ perm, const double* __restrict__ xp,
+                              double* __restrict__ x) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    x[perm[r]] = xp[r];
+}
+
 static int cg_variant() {
   static const int v = [] {
     const char* e = getenv("FVB_CG_VARIANT");
@@ -1438,6 +1461,27 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   CgParams prm{c->pattern(), c->team, A.V, A.crs, inv, b, x, r, z, pa, pb, q,
                S_SCR + 2, S_SCR + 3, S_SCR + 4, tol, abs_tol, max_iters,
                c->sync, c->partials, result};
+  // RCM order (patterns without stencil codes, one domain, 7-point rows):
+  // the solve runs on a permuted copy of the system
+  const bool rcm = c->rcm_perm && !c->teamed() && c->k == 7 && cg_variant() == -1;
+  double* xp = c->slot(S_SCR + 6);
+  if (rcm) {
+    if (!c->rcm_V) FVB_TRY(dalloc(c, &c->rcm_V, size_t(c->k) * size_t(c->nr)));
+    double* bp = c->slot(S_SCR + 7);
+    double* invp = c->slot(S_SCR + 8);
+    k_rcm_gather<7><<<grid_for(c->nr, 256), 256, 0, c->stream>>>(c->nr, c->rcm_perm, A.V, b, x, inv,
+                                                                c->rcm_V, bp, xp, invp);
+    note_launch();
+    FVB_CUDA(cudaGetLastError());
+    prm.P.I = c->rcm_I;
+    prm.P.diag_slot = c->rcm_ds;
+    prm.P.slot_face = nullptr;
+    prm.V = c->rcm_V;
+    prm.b = bp;
+    prm.x = xp;
+    prm.inv = invp;
+    c->cg_rcm_solves++;
+  }
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
   // FVB_CG_VARIANT selects an alternative kernel configuration (tuning
   // experiments, tools/cg_micro.py); the default is the measured best:
@@ -1481,6 +1525,11 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
       }
       break;
     default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
+  }
+  if (rcm) {
+    k_rcm_scatter<<<grid_for(c->nr, 256), 256, 0, c->stream>>>(c->nr, c->rcm_perm, xp, x);
+    note_launch();
+    FVB_CUDA(cudaGetLastError());
   }
   FVB_CUDA(cudaEventRecord(c->kev[1], c->stream));
   double h[9];

@@ -240,7 +240,7 @@ def test_stencil_code_dictionary():
     def codes_of(pat):
         ctx = context_for(None, None, pat)
         nc, ne = C.c_int(), C.c_int64()
-        _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(nc), C.byref(ne), None))
+        _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(nc), C.byref(ne), None, None))
         return nc.value, ne.value
 
     box = cases.box_mesh(10, 9, 8, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
@@ -270,3 +270,22 @@ def test_stencil_codes_bicgstab_bitwise_equals_explicit_indices(mode):
     assert out["-1"]["codes"] > 0 and out["20"]["codes"] == 0
     assert out["-1"]["x_sha"] == out["20"]["x_sha"]
     assert out["-1"]["iters"] == out["20"]["iters"] and out["-1"]["res"] == out["20"]["res"]
+
+
+def test_rcm_ordered_cg_on_renumbered_box():
+    # a randomly renumbered box has no stencil codes; CG then runs in the
+    # solver's reverse Cuthill-McKee order (>= 65536 rows).  Same row
+    # products, only the dot-product grouping moves: residual and iterate
+    # agree with the original-order solve (FVB_CG_VARIANT=22) to rounding
+    import json, os, subprocess, sys
+    root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
+    out = {}
+    for var in ("-1", "22"):
+        env = dict(os.environ, FVB_CG_VARIANT=var)
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "48", "80", "perm"],
+                             env=env, capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, res.stderr
+        out[var] = json.loads(res.stdout.strip().splitlines()[-1])
+    assert out["-1"]["codes"] == 0 and out["-1"]["rcm_solves"] == 3
+    assert out["22"]["rcm_solves"] == 0
+    assert abs(out["-1"]["res"] - out["22"]["res"]) <= 1e-9 * out["22"]["res"]

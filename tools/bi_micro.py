@@ -51,7 +51,7 @@ for rpt in range(3):
     res.append((r.wall_time, r.t_smvp, r.t_daxpy, r.t_reduction))
 t, ts, ta, tr = min(res)
 codes, nesc, defer = C.c_int(), C.c_int64(), C.c_int()
-_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer)))
+_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer), None))
 use_codes = codes.value and os.environ.get("FVB_BI_VARIANT", "-1") != "20"
 # the two SpMV passes read 1-byte stencil codes instead of K int32 indices
 row_bytes = 600.0 - (2 * (4 * K - 1) if use_codes else 0)

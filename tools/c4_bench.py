@@ -1,6 +1,7 @@
 """C4 timing: PISO on the perturbed + randomly renumbered 126^3 cavity
 (2,000,376 cells, BASELINE configs[3]); the renumbering leaves no common
-column-offset tuples, so the solvers run on explicit indices.  Device ms
+column-offset tuples, so the solvers run on explicit indices and CG in the
+solver's internal RCM order (FVB_CG_VARIANT=22: original order).  Device ms
 per step (CUDA events) and CG iterations.  Usage: python tools/c4_bench.py"""
 import ctypes as C, json, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
@@ -13,8 +14,8 @@ st = init_state(case, cfg)
 h = st._ctx.h
 for _ in range(2):
     piso_time_step(st, cfg)
-nc, ne = C.c_int(), C.c_int64()
-_lib.check(_lib.lib.fvb_pattern_codes(h, C.byref(nc), C.byref(ne), None))
+nc, ne, rcm = C.c_int(), C.c_int64(), C.c_int64()
+_lib.check(_lib.lib.fvb_pattern_codes(h, C.byref(nc), C.byref(ne), None, C.byref(rcm)))
 steps = 3
 n0 = len(st.residual_log)
 _lib.check(_lib.lib.fvb_sync(h))
@@ -26,4 +27,5 @@ _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
 cg = [r[3] for r in st.residual_log[n0:] if r[0] == "cg"]
 print(json.dumps({"workload": "C4 perturbed_cavity(126)", "cells": case.mesh.n_cells,
                   "ms_per_step": ms.value / steps, "cg_iters_per_step": sum(cg) / steps,
-                  "stencil_codes": nc.value, "escaped_rows": ne.value}))
+                  "stencil_codes": nc.value, "escaped_rows": ne.value,
+                  "cg_solves_in_rcm_order": rcm.value}))

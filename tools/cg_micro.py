@@ -1,8 +1,9 @@
 """CG kernel microbenchmark: fixed-iteration Jacobi-PCG on a cavity
 Laplacian-like SPD matrix (K = 7) through fvb_op_cg; prints device time per
 iteration and the algorithmic HBM rate (N(12K+96) bytes per iteration).
-Usage: python tools/cg_micro.py N ITERS [crs]  (FVB_CG_VARIANT selects the kernel; "crs"
-adds long-range couplings: CRS tail + escaped stencil-code rows)"""
+Usage: python tools/cg_micro.py N ITERS [crs|perm]  (FVB_CG_VARIANT selects the kernel;
+"crs" adds long-range couplings: CRS tail + escaped stencil-code rows; "perm"
+randomly renumbers the box: no stencil codes, RCM-ordered solve)"""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
@@ -12,7 +13,13 @@ from paper_1207_1571_b200.device import context_for
 n = int(sys.argv[1]); iters = int(sys.argv[2])
 t0 = time.time()
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
-if len(sys.argv) > 3 and sys.argv[3] == "crs":
+if len(sys.argv) > 3 and sys.argv[3] == "perm":
+    # randomly renumbered box: no stencil codes, the solver's RCM order applies
+    ni = mesh.n_internal
+    perm = np.random.default_rng(2).permutation(mesh.n_cells)
+    pairs = np.stack([perm[np.asarray(mesh.owner[:ni])], perm[np.asarray(mesh.neighbour)]], axis=1)
+    pat = sparse.pattern_from_pairs(mesh.n_cells, np.sort(pairs, axis=1), 16)
+elif len(sys.argv) > 3 and sys.argv[3] == "crs":
     # symmetric long-range couplings on ~2% of the rows with K capped at 7:
     # overflow entries go to the CRS tail, those rows escape the stencil codes
     ni = mesh.n_internal
@@ -36,6 +43,8 @@ rep = _lib.SolveReportC()
 P = _lib.ptr
 crs = np.full(max(pat.nnz_crs, 1), -1.0)
 setup = time.time() - t0
+rcm0 = C.c_int64()
+_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, None, None, None, C.byref(rcm0)))
 res = []
 for rpt in range(3):
     rc = _lib.lib.fvb_op_cg(ctx.h, P(_lib.f64(V)), P(crs), P(b), P(np.zeros(N)), P(x), 1e-300, 0.0,
@@ -44,7 +53,8 @@ for rpt in range(3):
     res.append((rep.wall_time, rep.t_smvp, rep.t_daxpy, rep.t_reduction))
 t, ta, tb, tr = min(res)
 codes, nesc, defer = C.c_int(), C.c_int64(), C.c_int()
-_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer)))
+rcm1 = C.c_int64()
+_lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer), C.byref(rcm1)))
 # 1-byte stencil codes replace the K int32 indices when the pattern compresses
 use_codes = codes.value and os.environ.get("FVB_CG_VARIANT", "-1") in ("-1", "22")
 # deferred x update (large systems): pass B no longer re-reads p
@@ -55,6 +65,6 @@ print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "-1"), "n": n, "it
                   "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
                   "us_reduce2x": 1e6 * tr / iters,
                   "alg_gbs": (setup_b + iters * bytes_it) / t / 1e9, "setup_s": round(setup, 1),
-                  "codes": codes.value if use_codes else 0, "defer_x": defer.value, "escaped": nesc.value if use_codes else 0,
+                  "codes": codes.value if use_codes else 0, "defer_x": defer.value, "rcm_solves": rcm1.value - rcm0.value, "escaped": nesc.value if use_codes else 0,
                   "nnz_crs": int(pat.nnz_crs), "res": rep.final_residual,
                   "x_sha": hashlib.sha256(x.tobytes()).hexdigest()[:16]}))
