@@ -221,7 +221,9 @@ struct Ctx {
   int* rcm_I = nullptr;
   int* rcm_ds = nullptr;
   double* rcm_V = nullptr;
+  double* rcm_vec = nullptr;  // BiCGStab: b', x' per component + 1/D'
   int64_t cg_rcm_solves = 0;
+  int64_t bi_rcm_solves = 0;
   int *crs_ptr = nullptr, *crs_col = nullptr, *crs_face = nullptr;
   // boundary conditions: 0 = u (3 comps), 1 = p
   uint8_t* bc_kind[2] = {nullptr, nullptr};

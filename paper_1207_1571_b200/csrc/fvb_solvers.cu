@@ -1426,6 +1426,34 @@ __global__ void k_rcm_scatter(int n, const int* __restrict__ perm, const double*
     x[perm[r]] = xp[r];
 }
 
+// RCM-ordered BiCGStab batch: the same gather / scatter for up to three
+// right-hand sides and solutions.
+struct RcmVecs {
+  const double* b[3];
+  double* x[3];
+  double* bp[3];
+  double* xp[3];
+};
+template <int KT>
+__global__ void k_rcm_gather_multi(int n, int ncomp, const int* __restrict__ perm,
+                                   const double* __restrict__ V, const double* __restrict__ inv,
+                                   double* __restrict__ Vp, double* __restrict__ invp, RcmVecs R) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int o = perm[r];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) Vp[size_t(s) * n + r] = V[size_t(s) * n + o];
+    invp[r] = inv[o];
+    for (int k = 0; k < ncomp; ++k) {
+      R.bp[k][r] = R.b[k][o];
+      R.xp[k][r] = R.x[k][o];
+    }
+  }
+}
+__global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ perm, RcmVecs R) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    for (int k = 0; k < ncomp; ++k) R.x[k][perm[r]] = R.xp[k][r];
+}
+
 static int cg_variant() {
   static const int v = [] {
     const char* e = getenv("FVB_CG_VARIANT");
@@ -1593,9 +1621,10 @@ static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const*
 // 3-pass kernel (default); FVB_BI_VARIANT=5 selects the 5-pass one
 template <int NC>
 static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const* x, double tol,
-                        double abs_tol, int max_iters, double* inv, double* result) {
+                        double abs_tol, int max_iters, double* inv, double* result,
+                        const PatternView* pov = nullptr) {
   Bi3Params<NC> prm;
-  prm.P = c->pattern();
+  prm.P = pov ? *pov : c->pattern();
   prm.T = c->team;
   prm.V = A.V;
   prm.crs = A.crs;
@@ -1664,6 +1693,37 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
       FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
     else
       FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
+  } else if (c->rcm_perm && !c->teamed() && c->k == 7 && !getenv("FVB_NO_RCM")) {
+    // renumbered mesh without stencil codes: solve in the RCM order (as CG)
+    if (!c->rcm_V) FVB_TRY(dalloc(c, &c->rcm_V, size_t(c->k) * size_t(c->nr)));
+    if (!c->rcm_vec) FVB_TRY(dalloc(c, &c->rcm_vec, size_t(7) * size_t(c->nr)));
+    RcmVecs R{};
+    double* bpp[3];
+    double* xpp[3];
+    for (int k = 0; k < ncomp; ++k) {
+      R.b[k] = b[k];
+      R.x[k] = x[k];
+      R.bp[k] = bpp[k] = c->rcm_vec + size_t(2 * k) * c->nr;
+      R.xp[k] = xpp[k] = c->rcm_vec + size_t(2 * k + 1) * c->nr;
+    }
+    double* invp = c->rcm_vec + size_t(6) * c->nr;
+    k_rcm_gather_multi<7><<<grid_for(c->nr, 256), 256, 0, c->stream>>>(
+        c->nr, ncomp, c->rcm_perm, A.V, inv, c->rcm_V, invp, R);
+    note_launch();
+    FVB_CUDA(cudaGetLastError());
+    PatternView P = c->pattern();
+    P.I = c->rcm_I;
+    P.diag_slot = c->rcm_ds;
+    P.slot_face = nullptr;
+    const MatView Ap{c->rcm_V, A.crs};
+    if (ncomp == 1)
+      FVB_TRY(bicg3_launch<1>(c, Ap, bpp, xpp, tol, abs_tol, max_iters, invp, result, &P));
+    else
+      FVB_TRY(bicg3_launch<3>(c, Ap, bpp, xpp, tol, abs_tol, max_iters, invp, result, &P));
+    k_rcm_scatter_multi<<<grid_for(c->nr, 256), 256, 0, c->stream>>>(c->nr, ncomp, c->rcm_perm, R);
+    note_launch();
+    FVB_CUDA(cudaGetLastError());
+    c->bi_rcm_solves++;
   } else {
     if (ncomp == 1)
       FVB_TRY(bicg3_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
