@@ -340,7 +340,7 @@ def _run_device_step(state, cfg, piso):
         msg = _lib.last_error().replace("{outer}", str(state.outer))
         if rc in (_lib.E_COUPLING,):
             raise CouplingError(msg)
-        _lib.check(rc)
+        raise _lib._ERR.get(rc, RuntimeError)(msg)
     state.add_wall("momentum_assembly", rep.t_momentum_assembly)
     state.add_wall("momentum_solve", rep.t_momentum_solve)
     state.add_wall("pressure_assembly", rep.t_pressure_assembly)

@@ -386,7 +386,7 @@ class RankRun(_TeamRunBase):
             msg = _lib.last_error().replace("{outer}", str(self.outer))
             if rc == _lib.E_COUPLING:
                 raise CouplingError(msg)
-            _lib.check(rc)
+            raise _lib._ERR.get(rc, RuntimeError)(msg)
         return float(rep.mom_res), float(rep.p_res)
 
     def piso_time_step(self, cfg):
