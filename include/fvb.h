@@ -328,12 +328,12 @@ int fvb_set_sm_share(fvb_ctx* ctx, int share);
  * bench/roofline evidence): n_codes distinct column-offset tuples of the
  * stencil-code compression (0 = off, the solvers read the explicit
  * indices), n_escape rows outside the dictionary, cg_defer_x = 1 when CG
- * folds x += alpha p into the next SpMV pass, cg_rcm_solves = CG solves run
- * so far in the solver's internal reverse Cuthill-McKee order (patterns
- * without stencil codes, e.g. randomly renumbered meshes).  Any pointer
- * may be NULL. */
+ * folds x += alpha p into the next SpMV pass, rcm_solves = CG and BiCGStab
+ * solves (a batch counts once) run so far in the solvers' internal reverse
+ * Cuthill-McKee order (patterns without stencil codes, e.g. randomly
+ * renumbered meshes).  Any pointer may be NULL. */
 int fvb_pattern_codes(fvb_ctx* ctx, int* n_codes, int64_t* n_escape, int* cg_defer_x,
-                      int64_t* cg_rcm_solves);
+                      int64_t* rcm_solves);
 
 /* number of kernels libfvb has launched in this process (bench evidence) */
 unsigned long long fvb_launch_count(void);

@@ -1530,12 +1530,12 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
 }
 
 int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape, int* cg_defer_x,
-                      int64_t* cg_rcm_solves) {
+                      int64_t* rcm_solves) {
   Ctx* c = &h->c;
   if (n_codes) *n_codes = c->scode ? c->n_scode : 0;
   if (n_escape) *n_escape = c->scode ? c->n_sescape : 0;
   if (cg_defer_x) *cg_defer_x = cg_defers_x(c) ? 1 : 0;
-  if (cg_rcm_solves) *cg_rcm_solves = c->cg_rcm_solves;
+  if (rcm_solves) *rcm_solves = c->cg_rcm_solves + c->bi_rcm_solves;
   return FVB_OK;
 }
 
