@@ -1,7 +1,7 @@
 """Benchmark: FP64 PISO time steps of the 3D lid-driven cavity on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c5|c2] [--n CELLS_PER_EDGE]
+                    [--config c5|c2] [--edge CELLS_PER_EDGE] [--no-aux]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
 
 Workload (default "C5", BASELINE.json configs[4] and the north-star target
@@ -68,7 +68,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cg-sample", type=int, default=20)
     ap.add_argument("--no-aux", action="store_true",
-                    help="skip the auxiliary C2 (128^3) measurement at N=1")
+                    help="skip the auxiliary C2 (128^3), C1/C3 and C4 measurements at N=1")
     return ap.parse_args()
 
 
@@ -606,7 +606,8 @@ def run_ours(args):
                               f"{counts['cg']:.0f}, BiCGStab {counts['bicgstab']:.0f} per step); "
                               f"OpenBLAS default threads; {d['sample_s']:.1f} s of CPU work"),
                    "s_per_step": d["s_per_step"]}
-    # ------------------------------------------- auxiliary C2 (configs[1])
+    # ------------------ auxiliary configs at N=1: C2 (configs[1]), C1/C3
+    # (configs[0], [2]) and C4 (configs[3], the renumbered 2M-cell mesh)
     aux = aux_small = aux_c4 = None
     if D.world == 1 and n != 128 and not args.no_aux:
         aux = measure_c2(steps=3, warmup=2)
