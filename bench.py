@@ -27,11 +27,15 @@ One JSON line on rank 0:
                CUDA-event duration; peak = MEASURED_PEAKS
                hbm_gbs x N GPUs; traffic = ncu DRAM bytes per launch scaled
                from profiles/ncu_k_cg_traffic.json
-  cpu_baseline the unmodified reference fvflow (baseline/_ref) on a bounded
-               sample: one piso_time_step on gen_cavity(min(n,128)) with CG
-               and BiCGStab capped, per-cell costs scaled to this workload
-               and to this run's iteration counts
---impl reference prints the reference arm's line (CPU, rank 0 only).
+  cpu_baseline the CPU path on a bounded sample (CpuSampler): the unmodified
+               reference fvflow when installed at baseline/_ref, else the
+               oracle port oracle/fvoracle.py ("kind" says which): PISO steps
+               of gen_cavity(min(n,64)) with CG and BiCGStab capped, under
+               "measured"; the per-step cost at this workload's cells and
+               this run's iteration counts under "extrapolated"
+--impl reference prints the reference arm's line (CPU, rank 0 only, never
+imports paper_1207_1571_b200): value = the extrapolated rate, ms_per_step =
+the measured bounded sample, plus a one-BLAS-thread figure.
 """
 
 import argparse
@@ -141,160 +145,214 @@ def make_case(n):
     return case
 
 
-# ------------------------------------------------------------ reference arm
-def _ref_modules():
-    if not os.path.isdir(os.path.join(REF_DIR, "fvflow")):
+# ------------------------------------------------------------ CPU baseline
+# Device-reported iteration counts per PISO step of C5 (gen_cavity(256),
+# max_iters 5000) from BENCH_r01 (20 timed steps after 5 warm-up steps):
+# the reference itself cannot run 256^3 here (~77 GB), and by the parity rule
+# its counts are within +-1 (CG) / +-2 (BiCGStab) per solve of these.
+C5_COUNTS = {"cg": 6296.4, "cg_solves": 2, "bicgstab": 357.15, "bicgstab_solves": 3}
+
+
+def reference_installed():
+    return os.path.isdir(os.path.join(REF_DIR, "fvflow"))
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max((i.get("num_threads", 1) for i in threadpool_info()
+                    if i.get("user_api") == "blas"), default=1)
+    except Exception:
         return None
-    if REF_DIR not in sys.path:
-        sys.path.insert(0, REF_DIR)
-    import fvflow.coupling as rc
-    import fvflow.fvm as rf
-    import fvflow.linsolve as rl
-    import fvflow.mesh as rm
-    import fvflow.sparse as rs
-    from fvflow.config import BoundarySpec, CaseConfig
-
-    return rc, rf, rl, rm, rs, BoundarySpec, CaseConfig
 
 
-class RefSampler:
-    """Bounded samples of the reference's own piso_time_step.
+class CpuSampler:
+    """Bounded samples of the CPU PISO step of gen_cavity(ns).
 
-    The reference objects are built from this package's setup arrays, which
-    are bit-identical to the reference's compute_geometry / build_pattern
-    (tests/test_native_setup.py); that skips 30-50 s of numpy setup.  One
-    sample = one reference step with CG capped at cg_cap and BiCGStab at
-    bi_cap iterations per solve: assembly and correction are timed in
-    full, the solver time per iteration is measured, and the step is
-    assembled from the target's iteration counts.  When the target mesh is
-    larger than the sample mesh, every term is scaled by the cell ratio
-    (numpy costs here are linear in N; SURVEY.md §6/§8(d) C5 prescribes
-    this extrapolation because 256^3 needs ~77 GB in the reference)."""
+    kind "reference": the unmodified reference package installed at
+    baseline/_ref, driven through its own API (fvflow.cases.gen_cavity,
+    coupling.init_state / piso_time_step, coupling.py:182-203, 356-370).
+    kind "port": when baseline/_ref is absent (the driver's fresh box), the
+    numpy restatement oracle/fvoracle.py (pinned bitwise/1e-12 against the
+    reference's golden vectors) on the oracle's own cavity generator
+    (oracle/fvcases.py).  Neither imports paper_1207_1571_b200.
 
-    def __init__(self, case, seed=None, cg_cap=20, bi_cap=10):
-        mods = _ref_modules()
-        self.ok = mods is not None
-        if not self.ok:
-            return
-        rc, rf, rl, rm, rs, BoundarySpec, CaseConfig = mods
-        from paper_1207_1571_b200 import mesh as pmesh, sparse as psparse
+    One sample = one PISO step from a fixed state (the state after one
+    capped step from rest), CG capped at cg_cap and BiCGStab at bi_cap
+    iterations per solve; assembly and corrections run in full.  What ran
+    is reported as measured; the per-step cost of a workload with other
+    iteration counts and cell counts is a separate, labelled model."""
 
-        self.rc, self.rs = rc, rs
-        m = case.mesh
-        rmesh = rm.Mesh(points=m.points, face_points=m.face_points, face_offsets=m.face_offsets,
-                        owner=m.owner, neighbour=m.neighbour,
-                        patches=[rm.Patch(p.name, p.kind, p.start, p.count) for p in m.patches],
-                        n_cells=m.n_cells)
-        g = pmesh.compute_geometry(m)
-        geom = rm.MeshGeometry(**{k: getattr(g, k) for k in g.__dataclass_fields__})
-        pp = psparse.build_pattern(m)
-        self.pat = rs.SparsityPattern(**{k: getattr(pp, k) for k in pp.__dataclass_fields__})
-        cc = CaseConfig(**{k: getattr(case.config, k) for k in case.config.__dataclass_fields__
-                           if k not in ("boundary", "samples")})
-        cc.boundary = {k: BoundarySpec(u=v.u, p=v.p) for k, v in case.config.boundary.items()}
-        self.cfg = rc.CouplingConfig.from_case_config(cc)
-        self.cfg.pressure.max_iters = cg_cap
-        self.cfg.momentum.max_iters = bi_cap
-        ub = {k: rf.bc_from_tuple(s.u) for k, s in cc.boundary.items()}
-        pb = {k: rf.bc_from_tuple(s.p) for k, s in cc.boundary.items()}
-        u = rf.make_vector("u", rmesh, ub)
-        p = rf.make_scalar("p", rmesh, pb)
-        if seed is not None:
-            u.values = seed["u"].copy()
-            p.values = seed["p"].copy()
-        rf.apply_bcs(u, geom, 0.0)
-        rf.apply_bcs(p, geom, 0.0)
-        flux = seed["flux"].copy() if seed is not None else rc._plain_flux(u, geom)
-        self.state = rc.RunState(mesh=rmesh, geom=geom, pattern=self.pat, u=u, p=p, flux=flux,
-                                 pin_pressure=True)
-        self.start = (u.values.copy(), p.values.copy(), flux.copy(),
-                      seed["outer"] if seed is not None else 1)
-        self.n = m.n_cells
-
-    def sample(self, counts, n_target):
-        rc, rs, st = self.rc, self.rs, self.state
-        st.u.values = self.start[0].copy()
-        st.p.values = self.start[1].copy()
-        st.flux = self.start[2].copy()
-        st.outer = self.start[3]
-        st.wall, st.residual_log = {}, []
-        A = rs.HybridMatrix.zeros(self.pat)
-        A.V[:] = 1.0
-        t = time.perf_counter()
-        rs.smvp(A, np.ones(self.n))
-        t_smvp = time.perf_counter() - t
+    def __init__(self, ns, cg_cap=20, bi_cap=10):
+        self.ns, self.n, self.caps = ns, ns ** 3, (cg_cap, bi_cap)
         t0 = time.perf_counter()
-        rc.piso_time_step(st, self.cfg)
-        t_sample = time.perf_counter() - t0
-        w = st.wall
-        cg_rows = [r for r in st.residual_log if r[0] == "cg"]
-        bi_rows = [r for r in st.residual_log if r[0] == "bicgstab"]
-        cg_it = sum(r[3] for r in cg_rows)
-        bi_it = sum(r[3] for r in bi_rows)
-        t_cg_iter = max(w.get("pressure_solve", 0.0) - len(cg_rows) * t_smvp, 0.0) / max(cg_it, 1)
-        t_bi_iter = max(w.get("momentum_solve", 0.0) - len(bi_rows) * t_smvp, 0.0) / max(bi_it, 1)
-        fixed = (w.get("momentum_assembly", 0.0) + w.get("pressure_assembly", 0.0)
-                 + w.get("correction", 0.0))
-        t_step = (fixed + counts["cg_solves"] * t_smvp + counts["cg"] * t_cg_iter
-                  + counts["bicgstab_solves"] * t_smvp + counts["bicgstab"] * t_bi_iter)
-        scale = n_target / self.n
-        return {"s_per_step": t_step * scale, "sample_s": t_sample, "t_cg_iter_s": t_cg_iter,
-                "t_bicgstab_iter_s": t_bi_iter, "t_smvp_s": t_smvp,
-                "assembly_correction_s": fixed, "sample_cells": self.n, "cell_scale": scale,
-                "sampled_iters": {"cg": cg_it, "bicgstab": bi_it}, "counts": counts,
-                "threads": os.environ.get("OPENBLAS_NUM_THREADS", "default")}
+        if reference_installed():
+            self.kind = "reference"
+            if REF_DIR not in sys.path:
+                sys.path.insert(0, REF_DIR)
+            import fvflow.cases as rcases
+            import fvflow.coupling as rc
+            import fvflow.sparse as rs
+
+            case = rcases.gen_cavity(ns)
+            case.config.algorithm, case.config.dt = "piso", 0.1 / ns
+            cfg = rc.CouplingConfig.from_case_config(case.config)
+            cfg.pressure.max_iters, cfg.momentum.max_iters = cg_cap, bi_cap
+            st = rc.init_state(case, cfg)
+            A = rs.HybridMatrix.zeros(st.pattern)
+            A.V[:] = 1.0
+            self._obj, self._step = st, (lambda: rc.piso_time_step(st, cfg))
+            self._spmv = lambda x: rs.smvp(A, x)
+            self._log = lambda: st.residual_log
+        else:
+            self.kind = "port"
+            if HERE not in sys.path:
+                sys.path.insert(0, HERE)
+            from oracle import fvcases
+            from oracle import fvoracle as O
+
+            mesh, cc = fvcases.cavity(ns)
+            run = O.Run(mesh, cc, iter_caps=(cg_cap, bi_cap))
+            A = O.Matrix(run.P)
+            A.V[:] = 1.0
+            self._obj, self._step = run, run.piso_step
+            self._spmv = lambda x: O.spmv(A, x)
+            self._log = lambda: run.log
+        self.setup_s = time.perf_counter() - t0
+        self.start = None
+
+    def _save(self):
+        o = self._obj
+        return (o.u.values.copy(), o.p.values.copy(), o.flux.copy(), o.outer)
+
+    def _restore(self, s):
+        o = self._obj
+        o.u.values, o.p.values, o.flux, o.outer = s[0].copy(), s[1].copy(), s[2].copy(), s[3]
+        o.wall.clear()
+        self._log().clear()
+
+    def sample(self):
+        """One bounded step; returns what was measured (seconds, iterations)."""
+        if self.start is None:  # first call: one capped step from rest
+            self._step()
+            self.start = self._save()
+        self._restore(self.start)
+        x = np.ones(self.n)
+        t = time.perf_counter()
+        self._spmv(x)
+        t_spmv = time.perf_counter() - t
+        t = time.perf_counter()
+        self._step()
+        wall_s = time.perf_counter() - t
+        w, log = self._obj.wall, self._log()
+        cg = [r[3] for r in log if r[0] == "cg"]
+        bi = [r[3] for r in log if r[0] == "bicgstab"]
+        solve_s = w.get("pressure_solve", 0.0) + w.get("momentum_solve", 0.0)
+        return {"wall_s": wall_s, "spmv_s": t_spmv, "cg_iters": sum(cg), "cg_solves": len(cg),
+                "bicgstab_iters": sum(bi), "bicgstab_solves": len(bi),
+                "pressure_solve_s": w.get("pressure_solve", 0.0),
+                "momentum_solve_s": w.get("momentum_solve", 0.0),
+                "assembly_correction_s": max(wall_s - solve_s, 0.0)}
+
+    @staticmethod
+    def model(samples, counts, n_sample, n_target):
+        """Per-step seconds of a workload with `counts` iterations per step on
+        n_target cells, from measured samples: each solve = one set-up SpMV
+        plus its iterations; per-iteration solver costs and the assembly +
+        correction cost are per cell and scaled linearly in cells (numpy
+        passes are streaming; on a 64^3 sample the vectors fit the host
+        caches better than at 256^3, so this model flatters the CPU)."""
+        m = lambda k: statistics.mean(s[k] for s in samples)  # noqa: E731
+        t_spmv = m("spmv_s")
+        t_cg = max(m("pressure_solve_s") - m("cg_solves") * t_spmv, 0.0) / max(m("cg_iters"), 1)
+        t_bi = (max(m("momentum_solve_s") - m("bicgstab_solves") * t_spmv, 0.0)
+                / max(m("bicgstab_iters"), 1))
+        fixed = m("assembly_correction_s")
+        s_step = (fixed + (counts["cg_solves"] + counts["bicgstab_solves"]) * t_spmv
+                  + counts["cg"] * t_cg + counts["bicgstab"] * t_bi)
+        scale = n_target / n_sample
+        return {"s_per_step": s_step * scale, "cell_scale": scale, "counts": counts,
+                "per_iteration_s_at_sample": {"cg": t_cg, "bicgstab": t_bi, "spmv": t_spmv},
+                "assembly_correction_s_at_sample": fixed,
+                "formula": ("(assembly+correction + (cg_solves+bicgstab_solves)*t_spmv + "
+                            "cg_iters*t_cg + bicgstab_iters*t_bicgstab) * n_target/n_sample")}
+
+    def measured(self, samples):
+        m = lambda k: statistics.mean(s[k] for s in samples)  # noqa: E731
+        return {"kind": self.kind, "mesh": f"gen_cavity({self.ns})", "cells": self.n,
+                "samples": len(samples), "s_per_sample": m("wall_s"),
+                "caps": {"cg": self.caps[0], "bicgstab": self.caps[1]},
+                "iters_per_sample": {"cg": m("cg_iters"), "bicgstab": m("bicgstab_iters")},
+                "setup_s": self.setup_s, "cpu_count": os.cpu_count(),
+                "blas_threads": blas_threads(),
+                "env_threads": {k: os.environ.get(k) for k in
+                                ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS") if os.environ.get(k)}}
+
+    def one_thread(self):
+        """One sample with BLAS limited to one thread."""
+        try:
+            from threadpoolctl import threadpool_limits
+        except Exception:
+            return None
+        with threadpool_limits(limits=1, user_api="blas"):
+            return self.sample()
 
 
-def _sample_case(n):
-    """The reference sample mesh: the workload itself up to 128^3, else 128^3."""
-    return make_case(min(n, 128))
+def sample_mesh(n):
+    """The CPU sample mesh: the workload itself up to 64^3, else 64^3."""
+    return min(n, 64)
 
 
-def _default_counts(n):
-    if n == 128:
-        return dict(REF_COUNTS_C2)
-    f = n / 128  # CG iterations grow ~2x per doubling of n (SURVEY.md §7)
-    return {"cg": int(3004 * f), "cg_solves": 2, "bicgstab": int(193 * f), "bicgstab_solves": 3}
+def cpu_label(kind):
+    return ("unmodified reference fvflow (baseline/_ref)" if kind == "reference" else
+            "oracle/fvoracle.py (numpy restatement of the reference, pinned to its golden "
+            "vectors; baseline/_ref not installed on this host)")
 
 
 def run_reference(args):
+    """The reference arm: the CPU implementation of the path on this host's
+    cores, on this arm's workload, metric and unit (rank 0 only)."""
     n = workload(args)
     N = n ** 3
-    counts = _default_counts(n)
-    sampler = RefSampler(_sample_case(n), cg_cap=args.cg_sample)
-    if not sampler.ok:
-        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref/fvflow not installed"}))
-        return
-    # warm-up: the CPU code has nothing to JIT; W SpMV calls touch the data
-    A = sampler.rs.HybridMatrix.zeros(sampler.pat)
+    counts = dict(C5_COUNTS) if n == 256 else (dict(REF_COUNTS_C2) if n == 128 else None)
+    if counts is None:
+        f = n / 128  # CG counts grow ~linearly in n on the cavity (SURVEY.md §7)
+        counts = {"cg": 3004 * f, "cg_solves": 2, "bicgstab": 193 * f, "bicgstab_solves": 3}
+    s = CpuSampler(sample_mesh(n), cg_cap=args.cg_sample)
     for _ in range(args.warmup):
-        sampler.rs.smvp(A, np.ones(sampler.n))
-    times = []
-    detail = None
-    for _ in range(args.steps):
-        d = sampler.sample(counts, N)
-        times.append(d["s_per_step"])
-        detail = d
-    ms = 1e3 * statistics.mean(times)
-    value = N / (ms / 1e3)
-    sample = (f"reference fvflow piso_time_step on gen_cavity({min(n, 128)}) from rest+1 step, "
-              f"CG capped at {args.cg_sample} and BiCGStab at 10 iterations per solve, assembly "
-              f"and correction timed in full; per-iteration costs scaled to CG {counts['cg']} / "
-              f"BiCGStab {counts['bicgstab']} iterations per step and by {N / sampler.n:g}x cells "
-              f"to gen_cavity({n})")
+        s.sample()
+    samples = [s.sample() for _ in range(args.steps)]
+    one = s.one_thread()
+    meas = s.measured(samples)
+    ext = CpuSampler.model(samples, counts, s.n, N)
+    ext_1t = CpuSampler.model([one], counts, s.n, N) if one else None
+    value = N / ext["s_per_step"]
+    sample = (f"{cpu_label(s.kind)}: PISO step of gen_cavity({s.ns}) from the state after one "
+              f"capped step from rest, CG capped at {s.caps[0]} and BiCGStab at {s.caps[1]} "
+              f"iterations per solve, assembly and correction in full, {args.steps} timed "
+              f"samples of {meas['s_per_sample']:.2f} s; value extrapolated to gen_cavity({n}) "
+              f"with {counts['cg']:.0f} CG + {counts['bicgstab']:.0f} BiCGStab iterations per "
+              f"step (model under 'extrapolated')")
     out = {
         "metric": METRIC, "impl": "reference",
         "value": value, "unit": "cell-updates/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "warmup": args.warmup,
+        # what actually ran per timed step (a bounded sample); value is the model
+        "ms_per_step": 1e3 * meas["s_per_sample"],
+        "value_basis": "extrapolated (see 'extrapolated'); ms_per_step is the measured sample",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (gen_cavity mesh, PISO)",
         "config": {"workload": f"gen_cavity({n}) PISO dt=0.1/{n}", "cells": N,
                    "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "cell-updates/s", "cores": os.cpu_count(),
-                         "kind": "reference", "sample": sample},
+                         "kind": s.kind, "sample": sample},
         "e2e": {"value": value, "unit": "cell-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "detail": detail,
+        "measured": meas,
+        "extrapolated": ext,
+        "one_thread": ({"value": N / ext_1t["s_per_step"], "s_per_step": ext_1t["s_per_step"],
+                        "sample_s": one["wall_s"]} if one else None),
     }
     print(json.dumps(out))
 
@@ -504,11 +562,6 @@ def run_ours(args):
     t_setup = time.perf_counter() - t_setup
     for _ in range(args.warmup):
         step()
-    seed = None
-    if D.world == 1 and not args.no_cpu_baseline:
-        seed = {"u": st.u.values.copy(), "p": st.p.values.copy(), "flux": st.flux.copy(),
-                "outer": st.outer}
-        st._dev.host_dirty.clear()
     clocks = ClockSampler(D.local) if D.rank == 0 else None
     nlog = len(log)
     l0 = _lib.lib.fvb_launch_count()
@@ -586,26 +639,23 @@ def run_ours(args):
                "ms_per_step": e2e_step}
     # ------------------------------------------------------- cpu baseline
     cpu = None
-    if seed is not None:
+    if D.world == 1 and not args.no_cpu_baseline:
         counts = {"cg": sum(cg_iters) / args.steps, "cg_solves": 2,
                   "bicgstab": sum(bi_iters) / args.steps, "bicgstab_solves": 3}
-        if n <= 128:
-            s = RefSampler(case, seed=seed, cg_cap=args.cg_sample)
-            where = "the same state as the timed steps"
-        else:
-            s = RefSampler(_sample_case(n), cg_cap=args.cg_sample)
-            where = f"rest on gen_cavity({min(n, 128)}), scaled by {N / min(n, 128) ** 3:g}x cells"
-        if s.ok:
-            d = s.sample(counts, N)
-            cpu = {"value": N / d["s_per_step"], "unit": "cell-updates/s",
-                   "cores": os.cpu_count(), "kind": "reference",
-                   "sample": (f"unmodified reference fvflow (baseline/_ref) piso_time_step from "
-                              f"{where}; CG capped at {args.cg_sample} and BiCGStab at 10 "
-                              f"iterations; assembly and correction timed in full, per-iteration "
-                              f"solver cost scaled to this run's mean counts (CG "
-                              f"{counts['cg']:.0f}, BiCGStab {counts['bicgstab']:.0f} per step); "
-                              f"OpenBLAS default threads; {d['sample_s']:.1f} s of CPU work"),
-                   "s_per_step": d["s_per_step"]}
+        s = CpuSampler(sample_mesh(n), cg_cap=args.cg_sample)
+        s.sample()  # warm-up (first call = the capped step from rest)
+        samples = [s.sample() for _ in range(3)]
+        meas = s.measured(samples)
+        ext = CpuSampler.model(samples, counts, s.n, N)
+        cpu = {"value": N / ext["s_per_step"], "unit": "cell-updates/s",
+               "cores": os.cpu_count(), "kind": s.kind,
+               "sample": (f"{cpu_label(s.kind)}: {len(samples)} PISO steps of "
+                          f"gen_cavity({s.ns}) with CG capped at {s.caps[0]} and BiCGStab at "
+                          f"{s.caps[1]} iterations per solve ({meas['s_per_sample']:.2f} s each, "
+                          f"assembly and correction in full); per-iteration costs scaled to this "
+                          f"run's mean counts (CG {counts['cg']:.0f}, BiCGStab "
+                          f"{counts['bicgstab']:.0f} per step) and by {ext['cell_scale']:g}x cells"),
+               "measured": meas, "extrapolated": ext}
     # ------------------ auxiliary configs at N=1: C2 (configs[1]), C1/C3
     # (configs[0], [2]) and C4 (configs[3], the renumbered 2M-cell mesh)
     aux = aux_small = aux_c4 = None

@@ -23,6 +23,7 @@ numpy's own ``@`` exactly as the reference does.
 """
 
 import math
+import time
 
 import numpy as np
 
@@ -564,7 +565,11 @@ def ddt(A, rhs, old, dt, g, coeff=1.0):
 class Run:
     """Coupled PISO/SIMPLE state (coupling.py:132-423), array-level restatement."""
 
-    def __init__(self, mesh, cc, pattern_override=None, geom_override=None):
+    def __init__(self, mesh, cc, pattern_override=None, geom_override=None, iter_caps=None):
+        # iter_caps = (cg, bicgstab) per-solve iteration caps (bench.py's bounded
+        # CPU samples); None = cc.max_iters for both, as the reference
+        self.caps = iter_caps or (cc.max_iters, cc.max_iters)
+        self.wall = {}  # coupling.py's RunState.wall sections (coupling.py:230-343)
         self.m = m = mesh_arrays(mesh)
         self.g = geom_override if geom_override is not None else geometry(m)
         self.P = pattern_override if pattern_override is not None else mesh_pattern(m)
@@ -590,6 +595,10 @@ class Run:
         fl[self.m["ni"]:][em] = 0.0
         return fl
 
+    def _tick(self, section, t0):
+        self.wall[section] = self.wall.get(section, 0.0) + time.perf_counter() - t0
+        return time.perf_counter()
+
     def _record(self, solver, name, rep):
         self.cum[solver] += rep[0]
         self.log.append((solver, name, self.outer, rep[0], rep[1], rep[2]))
@@ -597,17 +606,20 @@ class Run:
     # coupling.py:216-231
     def momentum_matrix(self, u_old=None):
         cc = self.cc
+        t0 = time.perf_counter()
         A = Matrix(self.P)
         rhs = np.zeros((self.m["nc"], 3))
         if u_old is not None:
             ddt(A, rhs, u_old, cc.dt, self.g)
         convection(A, rhs, self.flux, self.u, self.g, cc.convection)
         laplacian(A, rhs, cc.nu, self.u, self.g, cc.nonorth_correction, cc.limiter, coeff=-1.0)
+        self._tick("momentum_assembly", t0)
         return A, rhs
 
     # coupling.py:234-279
     def solve_momentum(self, A, b0, relax):
         cc = self.cc
+        t0 = time.perf_counter()
         dg = A.diag()
         gp = gradient(self.p, self.g)
         rhs = b0 - self.g["cell_volume"][:, None] * gp
@@ -622,16 +634,18 @@ class Run:
         worst = 0.0
         for c, name in enumerate(("ux", "uy", "uz")):
             x, rep = pbicgstab(As, rhs[:, c], self.u.values[:, c], cc.bicgstab_tol,
-                               max_iters=cc.max_iters)
+                               max_iters=self.caps[1])
             self.u.values[:, c] = x
             self._record("bicgstab", name, rep)
             worst = max(worst, rep[1] * float(bn[c]) / bs)
+        self._tick("momentum_solve", t0)
         return dg, worst
 
     # coupling.py:282-344
     def pressure_correct(self, A, b0, dg, relax_p):
         cc, m, g = self.cc, self.m, self.g
         u, p = self.u, self.p
+        t0 = time.perf_counter()
         au = np.stack([spmv(A, u.values[:, c]) for c in range(3)], axis=1)
         hv = u.values + (b0 - au) / dg[:, None]
         hb = BField(m, u.bcs, hv)
@@ -656,7 +670,9 @@ class Run:
                 dref = Ap.V[ref, ds]
                 rhs[ref] += dref * cc.pressure_ref_value
                 Ap.V[ref, ds] = 2.0 * dref
-            x, rep = pcg(Ap, rhs, p.values, cc.cg_tol, max_iters=cc.max_iters)
+            t0 = self._tick("pressure_assembly", t0)
+            x, rep = pcg(Ap, rhs, p.values, cc.cg_tol, max_iters=self.caps[0])
+            t0 = self._tick("pressure_solve", t0)
             self._record("cg", "p", rep)
             if first is None:
                 first = rep[1]
@@ -668,6 +684,7 @@ class Run:
         gp = gradient(p, g)
         u.values = hv - rau[:, None] * gp
         apply_bcs(u, g, self.t)
+        self._tick("correction", t0)
         return first
 
     def normalized(self, slot, res):
