@@ -324,10 +324,19 @@ int fvb_team_allreduce(fvb_ctx* ctx, double* vals, int m, int op);
  * of the SMs so every rank's solver kernel is co-resident */
 int fvb_set_sm_share(fvb_ctx* ctx, int share);
 
+/* solver data-format options of a context (no reference counterpart: the
+ * reference has one format).  Both give the same iterates: stencil codes
+ * read exactly the columns of the explicit indices (bitwise), and the RCM
+ * order keeps every row's products (only the dot-product grouping moves).
+ * Used by the format-equivalence tests and tools/cg_micro.py. */
+#define FVB_SOLVER_EXPLICIT_INDEX 1 /* SpMV passes read int32 indices, not stencil codes */
+#define FVB_SOLVER_NO_RCM 2         /* solve in the mesh order on renumbered meshes */
+int fvb_set_solver_options(fvb_ctx* ctx, int flags);
+
 /* solver data formats of the uploaded pattern (no reference counterpart;
  * bench/roofline evidence): n_codes distinct column-offset tuples of the
- * stencil-code compression (0 = off, the solvers read the explicit
- * indices), n_escape rows outside the dictionary, cg_defer_x = 1 when CG
+ * stencil-code compression (0 = off or FVB_SOLVER_EXPLICIT_INDEX set:
+ * the solvers read the explicit indices), n_escape rows outside the dictionary, cg_defer_x = 1 when CG
  * folds x += alpha p into the next SpMV pass, rcm_solves = CG and BiCGStab
  * solves (a batch counts once) run so far in the solvers' internal reverse
  * Cuthill-McKee order (patterns without stencil codes, e.g. randomly

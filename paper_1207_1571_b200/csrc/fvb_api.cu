@@ -1433,6 +1433,31 @@ int fvb_team_attach(fvb_ctx* h, int rank, int size, void* const* pool_bases,
     fvb_set_error("pool_bases[rank] is not this context's pool");
     return FVB_E_ARG;
   }
+  // peers on other devices (an in-process team over several GPUs, or IPC
+  // mappings): kernels store halos and mailbox words straight into their
+  // pools, so this device needs peer access to each of them
+  for (int q = 0; q < size; ++q) {
+    if (q == rank) continue;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, pool_bases[q]) != cudaSuccess) {
+      cudaGetLastError();
+      fvb_set_error("team rank %d: pool_bases[%d] is not a device pointer", rank, q);
+      return FVB_E_ARG;
+    }
+    if (at.type != cudaMemoryTypeDevice || at.device == c->dev) continue;
+    int ok = 0;
+    FVB_CUDA(cudaDeviceCanAccessPeer(&ok, c->dev, at.device));
+    if (!ok) {
+      fvb_set_error("team rank %d: device %d cannot access peer device %d (rank %d)", rank,
+                    c->dev, at.device, q);
+      return FVB_E_ARG;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(at.device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      cudaGetLastError();
+    else
+      FVB_CUDA(e);
+  }
   TeamView& T = c->team;
   T.rank = rank;
   T.size = size;
@@ -1529,11 +1554,21 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
   return run_step(c, cfg, u_speeds, rep, false);
 }
 
+int fvb_set_solver_options(fvb_ctx* h, int flags) {
+  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM)) {
+    fvb_set_error("unknown solver option bits 0x%x", flags);
+    return FVB_E_ARG;
+  }
+  h->c.solver_flags = flags;
+  return FVB_OK;
+}
+
 int fvb_pattern_codes(fvb_ctx* h, int* n_codes, int64_t* n_escape, int* cg_defer_x,
                       int64_t* rcm_solves) {
   Ctx* c = &h->c;
-  if (n_codes) *n_codes = c->scode ? c->n_scode : 0;
-  if (n_escape) *n_escape = c->scode ? c->n_sescape : 0;
+  const bool sc = uses_codes(c);
+  if (n_codes) *n_codes = sc ? c->n_scode : 0;
+  if (n_escape) *n_escape = sc ? c->n_sescape : 0;
   if (cg_defer_x) *cg_defer_x = cg_defers_x(c) ? 1 : 0;
   if (rcm_solves) *rcm_solves = c->cg_rcm_solves + c->bi_rcm_solves;
   return FVB_OK;

@@ -223,6 +223,7 @@ struct Ctx {
   double* rcm_V = nullptr;
   double* rcm_vec = nullptr;  // BiCGStab: b', x' per component + 1/D'
   int64_t cg_rcm_solves = 0;
+  int solver_flags = 0;      // FVB_SOLVER_* (fvb_set_solver_options)
   int64_t bi_rcm_solves = 0;
   int *crs_ptr = nullptr, *crs_col = nullptr, *crs_face = nullptr;
   // boundary conditions: 0 = u (3 comps), 1 = p
@@ -566,21 +567,15 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   // sys: the peers are other devices, so arrivals order this block's halo
   // stores at system scope
   const bool teamed = T.size > 1;
-  // Arrivals are ordered at GPU scope even in a multi-device team: a block's
-  // halo stores to peers precede its acq_rel.gpu arrival, that arrival
-  // precedes the last arriver's acquire, and the last arriver's fence.sc.sys
-  // before the mailbox flags is cumulative over everything in its causal
-  // past — so every halo store is visible to a peer that acquired the flag
-  // (PTX memory model: causality order is transitive across scopes).  A
-  // system-scope arrival for every block measured ~6 us more per reduction
-  // (profiles/r01_team.md).  FVB_TEAM_SCOPE=sys on the host plus
-  // FVB_ARRIVE_SYS=1 at build time restores it.
-#ifdef FVB_ARRIVE_SYS
+  // Multi-device team (T.sys): every block's arrival is a system-scope
+  // acq_rel, so its halo stores to the peers (NVLink) are ordered before the
+  // last arriver's mailbox flags by the release of the storing thread's own
+  // block — not only through the cumulativity of the last arriver's
+  // fence.sc.sys, which a gpu-scope arrival would rely on.  One device (all
+  // ranks co-resident, tests): gpu scope.  (A gpu-scope arrival measured
+  // ~6 us less per reduction on one device, profiles/r01_team.md, but a
+  // multi-GPU run has not validated it.)
   const bool sys = teamed && T.sys && sends;
-#else
-  const bool sys = false;
-  (void)sends;
-#endif
   block_reduce<M>(v, smem);
   volatile unsigned* vabort = sync + 2;
   double* bcast = reinterpret_cast<double*>(sync + 4);
@@ -692,9 +687,11 @@ enum SolveErr {
 // x must hold x0 on entry (ghost entries current); returns solution in x.
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol,
              double abs_tol, int max_iters, SolveOut* out);
-// true when cg_solve folds x += alpha p into the next pass A (default
-// kernel, 7-point rows)
+// true when cg_solve folds x += alpha p into the next pass A (7-point rows)
 bool cg_defers_x(const Ctx* c);
+// the solvers read stencil codes / run in RCM order (format options)
+bool uses_codes(const Ctx* c);
+bool uses_rcm(const Ctx* c);
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
                    double* const* x, double tol, double abs_tol, int max_iters,
                    SolveOut* out);

@@ -50,20 +50,10 @@ struct CgParams {
   double* result;  // [iters, converged, res0, res, err_kind, err_iter]
 };
 
-// Pass A with the ELL loads software-pipelined: the I/V slots of the
-// thread's next row are in flight while the current row gathers p and
-// sums (fixed K only; same arithmetic and order as ell_row).
-template <bool STREAM, typename T>
-__device__ __forceinline__ T ld_mat(const T* p) {
-  // matrix slots are read once per pass: evict-first keeps the gathered
-  // vectors resident in L1/L2
-  if (STREAM) return __ldcs(p);
-  return __ldg(p);
-}
-
-// Variant of the pipelined pass A that prefetches only the column indices
-// (the gather's address chain) DEPTH rows ahead; the values V of the current
-// row are loaded in-iteration (they are off the critical path).
+// Pass A with the column indices (the gather's address chain) prefetched
+// DEPTH rows ahead; the values V of the current row are loaded in-iteration
+// (they are off the critical path) with evict-first, so the gathered vectors
+// keep L1/L2.  Same arithmetic and order as ell_row.
 // load the index ring of the first DEPTH rows of a sweep
 template <int KT, int DEPTH>
 __device__ __forceinline__ void icols_ring_load(const PatternView& P, int (&cq)[DEPTH][KT], int i,
@@ -78,7 +68,7 @@ __device__ __forceinline__ void icols_ring_load(const PatternView& P, int (&cq)[
   }
 }
 
-template <int KT, int DEPTH, bool PRE>
+template <int KT, int DEPTH>
 __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const double* __restrict__ z,
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
@@ -93,9 +83,7 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
   const double* __restrict__ V = A.V;
   const bool team = T.size > 1;
   double acc = 0.0;
-  // PRE: the caller loaded the ring before the barrier that precedes this
-  // pass, so the first rows' address chain is already resolved
-  if (!PRE) icols_ring_load<KT, DEPTH>(P, cq, i, end, step);
+  icols_ring_load<KT, DEPTH>(P, cq, i, end, step);
   auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
   while (i < end) {
     double vi[KT];
@@ -216,75 +204,11 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
   return acc;
 }
 
-template <int KT, bool STREAM>
-__device__ __forceinline__ double cg_pass_a_pipe(const CgParams& A, const double* __restrict__ z,
-                                                 const double* __restrict__ po,
-                                                 double* __restrict__ pnew, double beta,
-                                                 bool first, int slot_new, int i, int end,
-                                                 int step) {
-  const PatternView& P = A.P;
-  const TeamView& T = A.T;
-  const int n = P.n;
-  const int* __restrict__ I = P.I;
-  const double* __restrict__ V = A.V;
-  const bool team = T.size > 1;
-  double acc = 0.0;
-  int ci[KT];
-  double vi[KT];
-  if (i < end) {
-#pragma unroll
-    for (int s = 0; s < KT; ++s) {
-      ci[s] = ld_mat<STREAM>(I + size_t(s) * n + i);
-      vi[s] = ld_mat<STREAM>(V + size_t(s) * n + i);
-    }
-  }
-  auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
-  while (i < end) {
-    const int nx = i + step;
-    int cn[KT];
-    double vn[KT];
-    if (nx < end) {
-#pragma unroll
-      for (int s = 0; s < KT; ++s) {
-        cn[s] = ld_mat<STREAM>(I + size_t(s) * n + nx);
-        vn[s] = ld_mat<STREAM>(V + size_t(s) * n + nx);
-      }
-    }
-    double pr[KT];
-#pragma unroll
-    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * g(ci[s] < 0 ? 0 : ci[s]);
-    double ev = pr[0];
-#pragma unroll
-    for (int s = 2; s < KT; s += 2) ev = ev + pr[s];
-    double y = ev;
-    if (KT > 1) {
-      double od = pr[1];
-#pragma unroll
-      for (int s = 3; s < KT; s += 2) od = od + pr[s];
-      y = ev + od;
-    }
-    const double qi = crs_tail(P, A.crs, i, y, g);
-    const double pi = g(i);
-    pnew[i] = pi;
-    A.q[i] = qi;
-    if (team && i >= T.n_inner) halo_send(T, i, slot_new, pi);
-    acc += pi * qi;
-#pragma unroll
-    for (int s = 0; s < KT; ++s) {
-      ci[s] = cn[s];
-      vi[s] = vn[s];
-    }
-    i = nx;
-  }
-  return acc;
-}
-
-// Row ownership: CONTIG = 0 grid-strides rows over all threads; CONTIG = 1
-// gives every block one contiguous chunk swept in blockDim steps, so the
-// +-1 and +-n neighbours a row gathers were loaded by the same SM moments
-// earlier (L1 hits) and only the +-n^2 ones come from L2.
-template <int KT, int THREADS, int MINB, int PIPE, int CONTIG = 0, int XB = 0, int PB2 = 0,
-          int SC = 0, int DF = 0>
+// KT > 0: fixed K, pass A with the index ring (cg_pass_a_icols) or, SC,
+// the stencil-code ring (cg_pass_a_codes), pass B on row pairs with 16-byte
+// L2-only loads; KT = 0: generic K, plain row loops.  Rows are grid-strided
+// over every thread (team_rows).
+template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
   // SC: stencil-coded pass A (PatternView::code) with the code table here
@@ -293,24 +217,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     for (int j = threadIdx.x; j < A.P.ncode * KT; j += blockDim.x) s_tab[j] = A.P.stab[j];
     __syncthreads();
   }
+  constexpr bool PB2 = KT > 0;
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int nrows = P.n;
-  int row0, n, G;
-  bool sends = T.size > 1;
   unsigned rnd = 0;  // reduction round of this launch (team_reduce)
-  if (CONTIG) {
-    const int chunk = ((nrows + gridDim.x - 1) / gridDim.x + 31) & ~31;
-    row0 = blockIdx.x * chunk + threadIdx.x;
-    n = min(nrows, (blockIdx.x + 1) * chunk);
-    G = blockDim.x;
-  } else {
-    const RowRange R = team_rows(T, nrows);
-    row0 = R.begin;
-    n = R.end;
-    G = R.step;
-    sends = R.sends;
-  }
+  const RowRange R = team_rows(T, nrows);
+  const int row0 = R.begin, n = R.end, G = R.step;
+  const bool sends = R.sends;
   const int tid = row0;
   const bool team = T.size > 1;
   const double* __restrict__ inv = A.inv;
@@ -356,15 +270,14 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
   const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
   constexpr int KR = KT > 0 ? KT : 1;
-  constexpr int DR = PIPE >= 4 ? PIPE - 2 : 1;
+  constexpr int DR = 2;  // rows of column indices in flight ahead of use
   // DEFER (DF): x += alpha p of iteration k runs in pass A of iteration
   // k + 1 (which holds that p as its old p), or in a final sweep — pass B
   // then streams r, q, 1/D and z only; same expression x + alpha p per row
-  constexpr bool DEFER = DF && (SC != 0 || PIPE >= 3) && KT > 0;
+  constexpr bool DEFER = DF && KT > 0;
   double alpha_prev = 0.0;
   const double* p_pend = nullptr;  // p whose x update is still pending
   int ring[DR][KR];
-  if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
   while (!conv && it < A.max_iters) {
     ++it;
     if (timer) tk = global_ns();
@@ -376,12 +289,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       if (SC && KT > 0) {
         pq[0] = cg_pass_a_codes<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab,
                                         DEFER ? A.x : nullptr, alpha_prev);
-      } else if (PIPE >= 3 && KT > 0) {
-        pq[0] = cg_pass_a_icols<KR, DR, (XB != 0)>(A, z, po, pnew, beta, first, slot_new, tid,
-                                                   n, G, ring, DEFER ? A.x : nullptr, alpha_prev);
-      } else if (PIPE && KT > 0) {
-        pq[0] = cg_pass_a_pipe<(KT > 0 ? KT : 1), (PIPE > 1)>(A, z, po, pnew, beta, first,
-                                                                slot_new, tid, n, G);
+      } else if (KT > 0) {
+        pq[0] = cg_pass_a_icols<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, ring,
+                                        DEFER ? A.x : nullptr, alpha_prev);
       } else {
         for (int i = tid; i < n; i += G) {
           auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
@@ -404,7 +314,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     // r -= alpha q, z = r / D, ||r||^2, r.z
     double s2[2] = {0.0, 0.0};
     int i_scalar = tid;
-    if (PB2 && !CONTIG && vec_ok) {
+    if (PB2 && vec_ok) {
       // two consecutive rows per thread with 16-byte loads/stores
       const int npair = n >> 1;
       for (int j = tid; j < npair; j += G) {
@@ -448,8 +358,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s2[0] += ri * ri;
       s2[1] += ri * zi;
     }
-    // next pass A's first index rows travel while this pass's reduction runs
-    if (XB) icols_ring_load<KR, DR>(P, ring, tid, n, G);
     if (timer) { const uint64_t t = global_ns(); t_axpy += t - tk; tk = t; }
     if (DEFER) {
       p_pend = pnew;
@@ -484,31 +392,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
 }
 
 // ------------------------------------------------------------ BiCGStab
-template <int NC>
-struct BiParams {
-  PatternView P;
-  TeamView T;
-  const double* V;
-  const double* crs;
-  const double* inv;
-  const double* b[NC];
-  double* x[NC];
-  double* r[NC];
-  double* rh[NC];
-  double* p[NC];
-  double* ph[NC];
-  double* v[NC];
-  double* s[NC];
-  double* sh[NC];
-  double* t[NC];
-  int slot_ph[NC], slot_sh[NC];  // pool slots (halo targets)
-  double tol, abs_tol;
-  int max_iters;
-  unsigned* sync;
-  double* partials;
-  double* result;  // per comp: [iters, converged, res0, res, err_kind, err_iter]
-};
-
 // y_c = A x_c for NC vectors sharing one pass over V and I.
 template <int KT, int NC, typename G>
 __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const double* __restrict__ V,
@@ -639,299 +522,12 @@ struct CompState {
   double bn, res0, res, rho, alpha, omega, beta, rr, rhr;
 };
 
-template <int KT, int NC, int THREADS = kSolverThreads, int MINB = 2>
-__global__ void __launch_bounds__(THREADS, MINB) k_bicgstab(BiParams<NC> A) {
-  __shared__ double red[32 * 2 * NC + 2 * NC];
-  __shared__ CompState S[NC];
-  const PatternView& P = A.P;
-  const TeamView& T = A.T;
-  const RowRange R = team_rows(T, P.n);
-  const int n = R.end;       // rows of this block: tid, tid + G, ... < n
-  const int G = R.step;
-  const int tid = R.begin;
-  const bool sends = R.sends;
-  unsigned rnd = 0;  // reduction round of this launch (team_reduce)
-  const bool team = T.size > 1;
-  const double* __restrict__ inv = A.inv;
-  bool act[NC];
-  bool timeout = false;
-
-  // setup (linsolve.py:180-196)
-  double sums[2 * NC];
-  {
-#pragma unroll
-    for (int m = 0; m < 2 * NC; ++m) sums[m] = 0.0;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) act[c] = true;
-    for (int i = tid; i < n; i += G) {
-      double ax[NC];
-      auto g = [&](int c, int col) { return A.x[c][col]; };
-      ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, ax);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double bi = A.b[c][i];
-        const double ri = bi - ax[c];
-        A.r[c][i] = ri;
-        A.rh[c][i] = ri;
-        sums[2 * c] += bi * bi;
-        sums[2 * c + 1] += ri * ri;
-      }
-    }
-  }
-  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, rnd, sends)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0)
-      for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
-    return;
-  }
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < NC; ++c) {
-      CompState& s = S[c];
-      s.it = 0; s.err = SE_NONE; s.err_it = 0; s.sconv = 0; s.restart = 0; s.copy = 0; s.live = 0;
-      s.bn = fmax(sqrt(sums[2 * c]), kResFloor);
-      s.res = sqrt(sums[2 * c + 1]) / s.bn;
-      s.res0 = s.res;
-      s.rr = sums[2 * c + 1];
-      s.rhr = s.rr;
-      s.done = s.res <= A.tol || s.res * s.bn <= A.abs_tol;
-      s.rho = s.alpha = s.omega = 1.0;
-      s.beta = 0.0;
-    }
-  }
-  __syncthreads();
-
-  uint64_t t_spmv = 0, t_axpy = 0, t_red = 0, tk = 0;
-  const bool timer = blockIdx.x == 0 && threadIdx.x == 0;
-  while (!timeout) {
-    if (timer) tk = global_ns();
-    // per-component scalar logic (linsolve.py:198-219), identical in every block
-    if (threadIdx.x == 0) {
-      for (int c = 0; c < NC; ++c) {
-        CompState& s = S[c];
-        s.sconv = 0;
-        s.live = 0;
-        if (s.done || s.err || s.it >= A.max_iters) continue;
-        s.it++;
-        double rho_new = s.it == 1 ? s.rr : s.rhr;
-        s.restart = fabs(rho_new) < kTiny;
-        if (s.restart) {
-          rho_new = s.rr;  // r_hat := r, so r_hat.r = ||r||^2
-          if (rho_new < kTiny) { s.err = SE_RHO; s.err_it = s.it; continue; }
-        }
-        s.copy = (s.it == 1 || s.restart);
-        if (!s.copy) s.beta = (rho_new / s.rho) * (s.alpha / s.omega);
-        s.rho = rho_new;
-        s.live = 1;
-      }
-    }
-    __syncthreads();
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      act[c] = S[c].live != 0;
-      any = any || act[c];
-    }
-    if (!any) break;
-    // pass P: p = r | p = (p - omega v) beta + r ; p_hat = p / D ; restart r_hat
-    for (int i = tid; i < n; i += G) {
-      const double iv = inv[i];
-      const bool snd = team && i >= T.n_inner;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (!act[c]) continue;
-        const double ri = A.r[c][i];
-        double pi;
-        if (S[c].copy) {
-          pi = ri;
-        } else {
-          pi = A.p[c][i] - S[c].omega * A.v[c][i];
-          pi = pi * S[c].beta;
-          pi = pi + ri;
-        }
-        A.p[c][i] = pi;
-        const double phi = pi * iv;
-        A.ph[c][i] = phi;
-        if (snd) halo_send(T, i, A.slot_ph[c], phi);
-        if (S[c].restart) A.rh[c][i] = ri;
-      }
-    }
-    if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-    {
-      double z1[1] = {0.0};
-      if (!team_reduce<1>(T, A.sync, A.partials, z1, red, rnd, sends)) { timeout = true; break; }
-    }
-    if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
-    // pass V: v = A p_hat, r_hat.v
-    {
-      double rv[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) rv[c] = 0.0;
-      auto g = [&](int c, int col) { return A.ph[c][col]; };
-      auto body = [&](int i, const double* y) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          if (!act[c]) continue;
-          A.v[c][i] = y[c];
-          rv[c] += A.rh[c][i] * y[c];
-        }
-      };
-      if (KT > 0) {
-        spmv_sweep<(KT > 0 ? KT : 1), NC>(P, A.V, A.crs, tid, n, G, act, g, body);
-      } else {
-        for (int i = tid; i < n; i += G) {
-          double y[NC];
-          ell_rows_multi<KT, NC>(P, A.V, A.crs, i, act, g, y);
-          body(i, y);
-        }
-      }
-      if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
-      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
-      if (threadIdx.x == 0)
-        for (int c = 0; c < NC; ++c) {
-          if (!act[c]) continue;
-          if (fabs(rv[c]) < kTiny) { S[c].err = SE_RV; S[c].err_it = S[c].it; continue; }
-          S[c].alpha = S[c].rho / rv[c];
-        }
-      __syncthreads();
-#pragma unroll
-      for (int c = 0; c < NC; ++c) act[c] = act[c] && !S[c].err;
-    }
-    // pass S: s = r - alpha v, s_hat = s / D, ||s||^2
-    {
-      double ss[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) ss[c] = 0.0;
-      for (int i = tid; i < n; i += G) {
-        const double iv = inv[i];
-        const bool snd = team && i >= T.n_inner;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          if (!act[c]) continue;
-          const double si = A.r[c][i] - S[c].alpha * A.v[c][i];
-          A.s[c][i] = si;
-          const double shi = si * iv;
-          A.sh[c][i] = shi;
-          if (snd) halo_send(T, i, A.slot_sh[c], shi);
-          ss[c] += si * si;
-        }
-      }
-      if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, ss, red, rnd, sends)) { timeout = true; break; }
-      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
-      if (threadIdx.x == 0)
-        for (int c = 0; c < NC; ++c) {
-          if (!act[c]) continue;
-          const double sn = sqrt(ss[c]);
-          if (sn / S[c].bn <= A.tol || sn <= A.abs_tol) {
-            S[c].sconv = 1;
-            S[c].res = sn / S[c].bn;
-          }
-        }
-      __syncthreads();
-    }
-    // pass T: converged-at-s components take x += alpha p_hat; others t = A s_hat
-    bool tact[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) tact[c] = act[c] && !S[c].sconv;
-    {
-      double tts[2 * NC];
-#pragma unroll
-      for (int m = 0; m < 2 * NC; ++m) tts[m] = 0.0;
-      auto g = [&](int c, int col) { return A.sh[c][col]; };
-      auto body = [&](int i, const double* y) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-          if (act[c] && S[c].sconv) A.x[c][i] = A.x[c][i] + S[c].alpha * A.ph[c][i];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          if (!tact[c]) continue;
-          A.t[c][i] = y[c];
-          tts[2 * c] += y[c] * y[c];
-          tts[2 * c + 1] += y[c] * A.s[c][i];
-        }
-      };
-      bool any_t = false;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) any_t = any_t || tact[c];
-      if (KT > 0 && any_t) {
-        spmv_sweep<(KT > 0 ? KT : 1), NC>(P, A.V, A.crs, tid, n, G, tact, g, body);
-      } else {
-        for (int i = tid; i < n; i += G) {
-          double y[NC];
-          ell_rows_multi<KT, NC>(P, A.V, A.crs, i, tact, g, y);
-          body(i, y);
-        }
-      }
-      if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, tts, red, rnd, sends)) { timeout = true; break; }
-      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
-      if (threadIdx.x == 0)
-        for (int c = 0; c < NC; ++c) {
-          if (!act[c]) continue;
-          if (S[c].sconv) { S[c].done = 1; continue; }
-          const double tt = tts[2 * c], ts = tts[2 * c + 1];
-          if (tt == 0.0) { S[c].err = SE_OMEGA; S[c].err_it = S[c].it; continue; }
-          S[c].omega = ts / tt;
-          if (fabs(S[c].omega) < kTiny) { S[c].err = SE_OMEGA; S[c].err_it = S[c].it; }
-        }
-      __syncthreads();
-#pragma unroll
-      for (int c = 0; c < NC; ++c) tact[c] = tact[c] && !S[c].err;
-    }
-    // pass X: x += alpha p_hat; x += omega s_hat; r = s - omega t; ||r||^2, r_hat.r
-    {
-      double rr[2 * NC];
-#pragma unroll
-      for (int m = 0; m < 2 * NC; ++m) rr[m] = 0.0;
-      for (int i = tid; i < n; i += G) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          if (!tact[c]) continue;
-          double xi = A.x[c][i] + S[c].alpha * A.ph[c][i];
-          xi = xi + S[c].omega * A.sh[c][i];
-          A.x[c][i] = xi;
-          const double ri = A.s[c][i] - S[c].omega * A.t[c][i];
-          A.r[c][i] = ri;
-          rr[2 * c] += ri * ri;
-          rr[2 * c + 1] += A.rh[c][i] * ri;
-        }
-      }
-      if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
-      if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
-      if (threadIdx.x == 0)
-        for (int c = 0; c < NC; ++c) {
-          if (!tact[c]) continue;
-          S[c].rr = rr[2 * c];
-          S[c].rhr = rr[2 * c + 1];
-          S[c].res = sqrt(rr[2 * c]) / S[c].bn;
-          if (!isfinite(S[c].res)) { S[c].err = SE_DIVERGED; S[c].err_it = S[c].it; continue; }
-          if (S[c].res <= A.tol || S[c].res * S[c].bn <= A.abs_tol) S[c].done = 1;
-        }
-      __syncthreads();
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    for (int c = 0; c < NC; ++c) {
-      A.result[6 * c + 0] = S[c].it;
-      A.result[6 * c + 1] = S[c].done ? 1.0 : 0.0;
-      A.result[6 * c + 2] = S[c].res0;
-      A.result[6 * c + 3] = S[c].res;
-      A.result[6 * c + 4] = timeout ? SE_TIMEOUT : S[c].err;
-      A.result[6 * c + 5] = S[c].err_it;
-    }
-    A.result[18] = 1e-9 * double(t_spmv);
-    A.result[19] = 1e-9 * double(t_axpy);
-    A.result[20] = 1e-9 * double(t_red);
-  }
-}
-
 // ------------------------------------------------------ BiCGStab, 3 passes
-// The same algorithm and rounding as k_bicgstab (linsolve.py:175-282) with
-// the vector passes fused away: p_hat and s_hat are never
+// Jacobi-PBiCGStab (linsolve.py:175-282) with the reference's five vector
+// passes fused into three: p_hat and s_hat are never
 // stored — every SpMV rebuilds them for the gathered columns from r, p, v
-// and 1/D exactly as the 5-pass kernel computes them, and the update pass
-// rebuilds them for the own row.  Three reductions per iteration: r_hat.v;
+// and 1/D with the reference's rounding (p_hat = p / D as linsolve.py
+// computes it), and the update pass rebuilds them for the own row.  Three reductions per iteration: r_hat.v;
 // ||s||^2, t.t, t.s (t is formed speculatively and dropped when s already
 // converged); ||r||^2, r_hat.r.  p and v are double-buffered because pass 1
 // gathers the previous ones while writing the new ones.  Decomposed runs
@@ -1454,20 +1050,17 @@ __global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ pe
     for (int k = 0; k < ncomp; ++k) R.x[k][perm[r]] = R.xp[k][r];
 }
 
-static int cg_variant() {
-  static const int v = [] {
-    const char* e = getenv("FVB_CG_VARIANT");
-    return e ? atoi(e) : -1;
-  }();
-  return v;
+bool uses_codes(const Ctx* c) {
+  return c->scode != nullptr && !(c->solver_flags & FVB_SOLVER_EXPLICIT_INDEX);
+}
+bool uses_rcm(const Ctx* c) {
+  return c->rcm_perm && !c->teamed() && c->k == 7 && !(c->solver_flags & FVB_SOLVER_NO_RCM);
 }
 
-// x += alpha p folded into the next pass A: 426.6 -> 398.4 us per
-// iteration at 16.8M rows, even at 2.1M (57.3 vs 56.9 us, one call;
+// x += alpha p folded into the next pass A on 7-point rows: 426.6 -> 398.4
+// us per iteration at 16.8M rows, even at 2.1M (57.3 vs 56.9 us, one call;
 // profiles/r01_cg_variants.md)
-bool cg_defers_x(const Ctx* c) {
-  return c->k == 7 && (cg_variant() == 22 || cg_variant() == -1);
-}
+bool cg_defers_x(const Ctx* c) { return c->k == 7; }
 
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double abs_tol,
              int max_iters, SolveOut* out) {
@@ -1491,7 +1084,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
                c->sync, c->partials, result};
   // RCM order (patterns without stencil codes, one domain, 7-point rows):
   // the solve runs on a permuted copy of the system
-  const bool rcm = c->rcm_perm && !c->teamed() && c->k == 7 && cg_variant() == -1;
+  const bool rcm = uses_rcm(c);
   double* xp = c->slot(S_SCR + 6);
   if (rcm) {
     if (!c->rcm_V) FVB_TRY(dalloc(c, &c->rcm_V, size_t(c->k) * size_t(c->nr)));
@@ -1511,48 +1104,25 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
     c->cg_rcm_solves++;
   }
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
-  // FVB_CG_VARIANT selects an alternative kernel configuration (tuning
-  // experiments, tools/cg_micro.py); the default is the measured best:
-  // pass A with the column indices prefetched two rows ahead (the gather's
-  // address chain), evict-first matrix loads, grid-strided rows, one
-  // 1024-thread block per SM, pass B on row pairs with 16-byte L2-only
-  // loads (profiles/r01_cg_variants.md).
-  const int variant = cg_variant();
+  // one 1024-thread block per SM; pass A on 1-byte stencil codes when the
+  // pattern has them, else on the explicit index ring (tuning history:
+  // profiles/r01_cg_variants.md)
+  const bool sc = uses_codes(c);
   switch (c->k) {
     case 5:
-      if (c->scode && variant != 20)
-        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1, 1>, prm, 1024, 1));
+      if (sc)
+        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 1>, prm, 1024, 1));
       else
-        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1));
+        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1>, prm, 1024, 1));
       break;
     case 7:
-      if (cg_defers_x(c)) {
-        // x update folded into pass A (profiles/r01_cg_variants.md)
-        if (c->scode)
-          FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 1, 1>, prm, 1024, 1));
-        else
-          FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 0, 1>, prm, 1024, 1));
-        break;
-      }
-      switch (variant) {
-        case 0: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 0>, prm)); break;     // plain pass A
-        case 9: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 2>, prm)); break;     // pipelined I/V
-        case 12: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4>, prm)); break;    // index ring, 2x512
-        case 18: FVB_TRY(coop_launch(c, k_cg<7, 512, 2, 4, 0, 1>, prm)); break;  // + ring across barrier
-        case 17: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4>, prm, 1024, 1)); break;  // scalar pass B
-        case 20: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1)); break;  // explicit I
-        case 22: FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 1, 1>, prm, 1024, 1)); break;  // codes + deferred x
-        default:
-          // stencil-coded rows when the pattern has codes (1 byte per row
-          // instead of K indices), else the explicit index ring
-          if (c->scode)
-            FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1, 1>, prm, 1024, 1));
-          else
-            FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 4, 0, 0, 1>, prm, 1024, 1));
-          break;
-      }
+      // x update folded into pass A (cg_defers_x)
+      if (sc)
+        FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 1, 1>, prm, 1024, 1));
+      else
+        FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 0, 1>, prm, 1024, 1));
       break;
-    default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2, 0>, prm)); break;
+    default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2>, prm)); break;
   }
   if (rcm) {
     k_rcm_scatter<<<grid_for(c->nr, 256), 256, 0, c->stream>>>(c->nr, c->rcm_perm, xp, x);
@@ -1581,44 +1151,6 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   return FVB_OK;
 }
 
-template <int NC>
-static int bicg_launch(Ctx* c, MatView A, const double* const* b, double* const* x, double tol,
-                       double abs_tol, int max_iters, double* inv, double* result) {
-  BiParams<NC> prm;
-  prm.P = c->pattern();
-  prm.T = c->team;
-  prm.V = A.V;
-  prm.crs = A.crs;
-  prm.inv = inv;
-  int s = S_SCR + 1;
-  for (int k = 0; k < NC; ++k) {
-    prm.b[k] = b[k];
-    prm.x[k] = x[k];
-    prm.r[k] = c->slot(s++);
-    prm.rh[k] = c->slot(s++);
-    prm.p[k] = c->slot(s++);
-    prm.slot_ph[k] = s;
-    prm.ph[k] = c->slot(s++);
-    prm.v[k] = c->slot(s++);
-    prm.s[k] = c->slot(s++);
-    prm.slot_sh[k] = s;
-    prm.sh[k] = c->slot(s++);
-    prm.t[k] = c->slot(s++);
-  }
-  prm.tol = tol;
-  prm.abs_tol = abs_tol;
-  prm.max_iters = max_iters;
-  prm.sync = c->sync;
-  prm.partials = c->partials;
-  prm.result = result;
-  switch (c->k) {
-    case 5: return coop_launch(c, k_bicgstab<5, NC>, prm);
-    case 7: return coop_launch(c, k_bicgstab<7, NC>, prm);
-    default: return coop_launch(c, k_bicgstab<0, NC>, prm);
-  }
-}
-
-// 3-pass kernel (default); FVB_BI_VARIANT=5 selects the 5-pass one
 template <int NC>
 static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const* x, double tol,
                         double abs_tol, int max_iters, double* inv, double* result,
@@ -1651,13 +1183,9 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   prm.sync = c->sync;
   prm.partials = c->partials;
   prm.result = result;
-  static const int variant = [] {
-    const char* e = getenv("FVB_BI_VARIANT");
-    return e ? atoi(e) : -1;
-  }();
-  // stencil-coded SpMV sweeps when the pattern has codes (FVB_BI_VARIANT=20:
-  // explicit indices)
-  const bool sc = c->scode && variant != 20;
+  // stencil-coded SpMV sweeps when the pattern has codes (unless the
+  // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX)
+  const bool sc = uses_codes(c);
   switch (c->k) {
     case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm)
                       : coop_launch(c, k_bicgstab3<5, NC>, prm);
@@ -1684,16 +1212,7 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
     return FVB_E_ARG;
   }
   FVB_CUDA(cudaEventRecord(c->kev[0], c->stream));
-  static const bool five = [] {
-    const char* e = getenv("FVB_BI_VARIANT");
-    return e && atoi(e) == 5;
-  }();
-  if (five) {
-    if (ncomp == 1)
-      FVB_TRY(bicg_launch<1>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
-    else
-      FVB_TRY(bicg_launch<3>(c, A, b, x, tol, abs_tol, max_iters, inv, result));
-  } else if (c->rcm_perm && !c->teamed() && c->k == 7 && !getenv("FVB_NO_RCM")) {
+  if (uses_rcm(c)) {
     // renumbered mesh without stencil codes: solve in the RCM order (as CG)
     if (!c->rcm_V) FVB_TRY(dalloc(c, &c->rcm_V, size_t(c->k) * size_t(c->nr)));
     if (!c->rcm_vec) FVB_TRY(dalloc(c, &c->rcm_vec, size_t(7) * size_t(c->nr)));

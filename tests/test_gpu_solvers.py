@@ -211,25 +211,23 @@ def test_bicgstab_batch_kernel_on_box_operators(n, crs_tail):
 @pytest.mark.parametrize("mode", ["", "crs"])
 def test_stencil_codes_cg_bitwise_equals_explicit_indices(mode):
     # pass A on 1-byte stencil codes reads exactly the columns of the
-    # explicit index array: same iterates, bit for bit (FVB_CG_VARIANT=20
-    # forces the explicit-index kernel); "crs": escaped rows + CRS tail
+    # explicit index array: same iterates, bit for bit ("explicit" sets
+    # FVB_SOLVER_EXPLICIT_INDEX); "crs": escaped rows + CRS tail
     import json, os, subprocess, sys
     root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
     out = {}
-    for var in ("-1", "20", "22"):  # 22: codes + x update deferred into pass A
-        env = dict(os.environ, FVB_CG_VARIANT=var)
-        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "24", "60", mode],
-                             env=env, capture_output=True, text=True, timeout=600)
+    for var in ("codes", "explicit"):
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "24", "60",
+                              mode or "box", var], capture_output=True, text=True, timeout=600)
         assert res.returncode == 0, res.stderr
         out[var] = json.loads(res.stdout.strip().splitlines()[-1])
     if mode:
-        assert out["-1"]["escaped"] > 0 and out["-1"]["nnz_crs"] > 0
+        assert out["codes"]["escaped"] > 0 and out["codes"]["nnz_crs"] > 0
     else:
-        assert out["-1"]["codes"] == 27 and out["-1"]["escaped"] == 0
-    assert out["20"]["codes"] == 0
-    for var in ("-1", "22"):
-        assert out[var]["x_sha"] == out["20"]["x_sha"]
-        assert out[var]["res"] == out["20"]["res"]
+        assert out["codes"]["codes"] == 27 and out["codes"]["escaped"] == 0
+    assert out["explicit"]["codes"] == 0 and out["codes"]["defer_x"] == 1
+    assert out["codes"]["x_sha"] == out["explicit"]["x_sha"]
+    assert out["codes"]["res"] == out["explicit"]["res"]
 
 
 def test_stencil_code_dictionary():
@@ -255,40 +253,40 @@ def test_stencil_code_dictionary():
 
 @pytest.mark.parametrize("mode", ["", "crs"])
 def test_stencil_codes_bicgstab_bitwise_equals_explicit_indices(mode):
-    # batched BiCGStab SpMV sweeps on stencil codes (FVB_BI_VARIANT=20 forces
-    # the explicit indices); "crs" adds rows that overflow K (escaped rows
-    # and a CRS tail)
+    # batched BiCGStab SpMV sweeps on stencil codes ("explicit" sets
+    # FVB_SOLVER_EXPLICIT_INDEX); "crs" adds rows that overflow K (escaped
+    # rows and a CRS tail)
     import json, os, subprocess, sys
     root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
     out = {}
-    for var in ("-1", "20"):
-        env = dict(os.environ, FVB_BI_VARIANT=var)
-        res = subprocess.run([sys.executable, os.path.join(root, "tools", "bi_micro.py"), "20", "30", mode],
-                             env=env, capture_output=True, text=True, timeout=600)
+    for var in ("codes", "explicit"):
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "bi_micro.py"), "20", "30",
+                              mode or "box", var], capture_output=True, text=True, timeout=600)
         assert res.returncode == 0, res.stderr
         out[var] = json.loads(res.stdout.strip().splitlines()[-1])
-    assert out["-1"]["codes"] > 0 and out["20"]["codes"] == 0
-    assert out["-1"]["x_sha"] == out["20"]["x_sha"]
-    assert out["-1"]["iters"] == out["20"]["iters"] and out["-1"]["res"] == out["20"]["res"]
+    assert out["codes"]["codes"] > 0 and out["explicit"]["codes"] == 0
+    assert out["codes"]["x_sha"] == out["explicit"]["x_sha"]
+    assert out["codes"]["iters"] == out["explicit"]["iters"]
+    assert out["codes"]["res"] == out["explicit"]["res"]
 
 
 def test_rcm_ordered_cg_on_renumbered_box():
     # a randomly renumbered box has no stencil codes; CG then runs in the
     # solver's reverse Cuthill-McKee order (>= 65536 rows).  Same row
     # products, only the dot-product grouping moves: residual and iterate
-    # agree with the original-order solve (FVB_CG_VARIANT=22) to rounding
+    # agree with the original-order solve ("norcm" sets FVB_SOLVER_NO_RCM)
+    # to rounding
     import json, os, subprocess, sys
     root = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..")
     out = {}
-    for var in ("-1", "22"):
-        env = dict(os.environ, FVB_CG_VARIANT=var)
-        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "48", "80", "perm"],
-                             env=env, capture_output=True, text=True, timeout=900)
+    for var in ("rcm", "norcm"):
+        res = subprocess.run([sys.executable, os.path.join(root, "tools", "cg_micro.py"), "48", "80", "perm",
+                              var], capture_output=True, text=True, timeout=900)
         assert res.returncode == 0, res.stderr
         out[var] = json.loads(res.stdout.strip().splitlines()[-1])
-    assert out["-1"]["codes"] == 0 and out["-1"]["rcm_solves"] == 3
-    assert out["22"]["rcm_solves"] == 0
-    assert abs(out["-1"]["res"] - out["22"]["res"]) <= 1e-9 * out["22"]["res"]
+    assert out["rcm"]["codes"] == 0 and out["rcm"]["rcm_solves"] == 3
+    assert out["norcm"]["rcm_solves"] == 0
+    assert abs(out["rcm"]["res"] - out["norcm"]["res"]) <= 1e-9 * out["norcm"]["res"]
 
 
 def test_rcm_ordered_bicgstab_single_and_batched():

@@ -2,8 +2,10 @@
 Jacobi-BiCGStab on a convection-diffusion-like nonsymmetric matrix (K = 7)
 through fvb_op_bicgstab_batched; prints device time per batched iteration
 and the algorithmic HBM rate (600 B per row per batched iteration).
-Usage: python tools/bi_micro.py N ITERS [crs]  (FVB_BI_VARIANT selects the kernel;
-"crs" adds long-range couplings that spill into the CRS tail)"""
+Usage: python tools/bi_micro.py N ITERS [crs] [explicit]
+"crs" adds long-range couplings that spill into the CRS tail; "explicit"
+makes the SpMV sweeps read int32 indices instead of stencil codes
+(fvb_set_solver_options)."""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
@@ -11,8 +13,9 @@ from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
 
 n = int(sys.argv[1]); iters = int(sys.argv[2])
+opts = _lib.SOLVER_EXPLICIT_INDEX if "explicit" in sys.argv[3:] else 0
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
-crs_mode = len(sys.argv) > 3 and sys.argv[3] == "crs"
+crs_mode = "crs" in sys.argv[3:]
 if crs_mode:
     # extra long-range couplings on ~2% of the rows with K capped at 7: the
     # overflow entries go to the CRS tail
@@ -40,6 +43,7 @@ V[np.arange(N), pat.diag_slot] = -V.sum(axis=1) - tail + 0.05
 b = np.random.default_rng(0).normal(size=3 * N)
 x = np.empty(3 * N)
 ctx = context_for(None, None, pat)
+_lib.check(_lib.lib.fvb_set_solver_options(ctx.h, opts))
 reps = (_lib.SolveReportC * 3)()
 P = _lib.ptr
 res = []
@@ -52,11 +56,11 @@ for rpt in range(3):
 t, ts, ta, tr = min(res)
 codes, nesc, defer = C.c_int(), C.c_int64(), C.c_int()
 _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer), None))
-use_codes = codes.value and os.environ.get("FVB_BI_VARIANT", "-1") != "20"
+use_codes = codes.value > 0
 # the two SpMV passes read 1-byte stencil codes instead of K int32 indices
 row_bytes = 600.0 - (2 * (4 * K - 1) if use_codes else 0)
 it = reps[0].iterations
-print(json.dumps({"variant": os.environ.get("FVB_BI_VARIANT", "-"), "n": n, "k": int(K),
+print(json.dumps({"options": opts, "n": n, "k": int(K),
                   "nnz_crs": int(pat.nnz_crs),
                   "iters": [reps[c].iterations for c in range(3)],
                   "err": [reps[c].error_kind for c in range(3)] if hasattr(reps[0], "error_kind") else None,

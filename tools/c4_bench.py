@@ -1,8 +1,9 @@
 """C4 timing: PISO on the perturbed + randomly renumbered 126^3 cavity
 (2,000,376 cells, BASELINE configs[3]); the renumbering leaves no common
 column-offset tuples, so the solvers run on explicit indices and CG in the
-solver's internal RCM order (FVB_CG_VARIANT=22: original order).  Device ms
-per step (CUDA events) and CG iterations.  Usage: python tools/c4_bench.py"""
+solver's internal RCM order ("norcm": original order, FVB_SOLVER_NO_RCM).
+Device ms per step (CUDA events) and CG iterations.
+Usage: python tools/c4_bench.py [norcm]"""
 import ctypes as C, json, os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 from paper_1207_1571_b200 import _lib, cases
@@ -12,6 +13,8 @@ case = cases.perturbed_cavity(126)
 cfg = CouplingConfig.from_case_config(case.config)
 st = init_state(case, cfg)
 h = st._ctx.h
+if "norcm" in sys.argv[1:]:
+    _lib.check(_lib.lib.fvb_set_solver_options(h, _lib.SOLVER_NO_RCM))
 for _ in range(2):
     piso_time_step(st, cfg)
 nc, ne, rcm = C.c_int(), C.c_int64(), C.c_int64()

@@ -1,9 +1,11 @@
 """CG kernel microbenchmark: fixed-iteration Jacobi-PCG on a cavity
 Laplacian-like SPD matrix (K = 7) through fvb_op_cg; prints device time per
 iteration and the algorithmic HBM rate (N(12K+96) bytes per iteration).
-Usage: python tools/cg_micro.py N ITERS [crs|perm]  (FVB_CG_VARIANT selects the kernel;
+Usage: python tools/cg_micro.py N ITERS [crs|perm] [explicit] [norcm]
 "crs" adds long-range couplings: CRS tail + escaped stencil-code rows; "perm"
-randomly renumbers the box: no stencil codes, RCM-ordered solve)"""
+randomly renumbers the box: no stencil codes, RCM-ordered solve; "explicit"
+and "norcm" set the context's solver format options (fvb_set_solver_options:
+explicit int32 indices instead of stencil codes / mesh order instead of RCM)."""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
@@ -11,6 +13,8 @@ from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
 
 n = int(sys.argv[1]); iters = int(sys.argv[2])
+opts = (_lib.SOLVER_EXPLICIT_INDEX if "explicit" in sys.argv[3:] else 0) | \
+    (_lib.SOLVER_NO_RCM if "norcm" in sys.argv[3:] else 0)
 t0 = time.time()
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
 if len(sys.argv) > 3 and sys.argv[3] == "perm":
@@ -39,6 +43,7 @@ V[np.arange(N), pat.diag_slot] = (pat.I >= 0).sum(axis=1) - 1 + ncrs + 0.01
 b = np.random.default_rng(0).normal(size=N)
 x = np.empty(N)
 ctx = context_for(None, None, pat)
+_lib.check(_lib.lib.fvb_set_solver_options(ctx.h, opts))
 rep = _lib.SolveReportC()
 P = _lib.ptr
 crs = np.full(max(pat.nnz_crs, 1), -1.0)
@@ -56,11 +61,11 @@ codes, nesc, defer = C.c_int(), C.c_int64(), C.c_int()
 rcm1 = C.c_int64()
 _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, C.byref(codes), C.byref(nesc), C.byref(defer), C.byref(rcm1)))
 # 1-byte stencil codes replace the K int32 indices when the pattern compresses
-use_codes = codes.value and os.environ.get("FVB_CG_VARIANT", "-1") in ("-1", "22")
+use_codes = codes.value > 0
 # deferred x update (large systems): pass B no longer re-reads p
 bytes_it = N * ((8 * K + 1 if use_codes else 12 * K) + (88 if defer.value else 96))
 setup_b = N * (12 * K + 80)
-print(json.dumps({"variant": os.environ.get("FVB_CG_VARIANT", "-1"), "n": n, "iters": rep.iterations,
+print(json.dumps({"options": opts, "n": n, "iters": rep.iterations,
                   "us_per_iter": 1e6 * t / iters,
                   "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
                   "us_reduce2x": 1e6 * tr / iters,
