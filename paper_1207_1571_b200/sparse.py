@@ -182,28 +182,36 @@ class HybridMatrix:
         np.add.at(self.crs_val, addr[~e] - split, values[~e])
 
     def to_dense(self):
+        """Dense copy (debugging and small-case tests only)."""
         p = self.pattern
-        d = np.zeros((p.n, p.n))
-        r, c = np.nonzero(p.I >= 0)
-        d[r, p.I[r, c]] = self.V[r, c]
-        d[p.crs_row, p.crs_col] = self.crs_val
-        return d
+        out = np.zeros((p.n, p.n))
+        live = p.I >= 0
+        out[np.nonzero(live)[0], p.I[live]] = self.V[live]
+        if p.nnz_crs:
+            out[p.crs_row, p.crs_col] = self.crs_val
+        return out
+
+
+def _slot_of(p, addr):
+    """(value array, index) behind a flat address: ELL slots first, then the
+    CRS tail (the address space of sparse.py:158)."""
+    addr = int(addr)
+    ell = p.n * p.k
+    if 0 <= addr < ell:
+        i, s = divmod(addr, p.k)
+        if p.I[i, s] < 0:
+            raise SparseError(f"address {addr} points at a padding sentinel")
+        return "V", (i, s)
+    if ell <= addr < ell + p.nnz_crs:
+        return "crs_val", addr - ell
+    raise SparseError(f"address {addr} outside pattern")
 
 
 def coeff_accumulate(A, addr, value, add=True):
-    """Checked single-entry set/increment (sparse.py:269-288)."""
-    p = A.pattern
-    split = p.n * p.k
-    if 0 <= addr < split:
-        i, s = divmod(int(addr), p.k)
-        if p.I[i, s] < 0:
-            raise SparseError(f"address {addr} points at a padding sentinel")
-        A.V[i, s] = A.V[i, s] + value if add else value
-    elif split <= addr < split + p.nnz_crs:
-        q = int(addr) - split
-        A.crs_val[q] = A.crs_val[q] + value if add else value
-    else:
-        raise SparseError(f"address {addr} outside pattern")
+    """Checked single-entry add (or set, add=False) (sparse.py:269-288)."""
+    name, at = _slot_of(A.pattern, addr)
+    arr = getattr(A, name)
+    arr[at] = arr[at] + value if add else value
 
 
 def diagonal(A):
@@ -288,17 +296,18 @@ def unpack_q(q, n, k, mode="by_N"):
 
 
 def format_debug(A):
-    """Human-readable dump of a small matrix (reference sparse.py:366-383)."""
+    """Text dump of a small matrix: dense rows, then I, J, V and the CRS
+    tail (reference sparse.py:366-383 content)."""
     p = A.pattern
     if p.n > 16:
         raise SparseError("debug dump limited to n <= 16")
-    lines = [f"hybrid {p.n}x{p.n}, K={p.k}, crs entries: {p.nnz_crs}"]
-    for row in A.to_dense():
-        lines.append("  [" + " ".join(f"{v:10.4g}" for v in row) + "]")
-    lines.append(f"I = {p.I.tolist()}")
-    lines.append(f"J = {p.J.tolist()}")
-    lines.append(f"V = {np.round(A.V, 6).tolist()}")
+    dense = A.to_dense()
+    parts = [f"hybrid {p.n}x{p.n}, K={p.k}, crs entries: {p.nnz_crs}"]
+    parts += ["  [" + " ".join(format(v, "10.4g") for v in row) + "]" for row in dense]
+    for label, arr in (("I", p.I), ("J", p.J)):
+        parts.append(f"{label} = {arr.tolist()}")
+    parts.append("V = %s" % np.round(A.V, 6).tolist())
     if p.nnz_crs:
-        lines.append(f"CRS rows {p.crs_row.tolist()} cols {p.crs_col.tolist()} "
-                     f"vals {np.round(A.crs_val, 6).tolist()}")
-    return "\n".join(lines)
+        parts.append("CRS rows %s cols %s vals %s" % (p.crs_row.tolist(), p.crs_col.tolist(),
+                                                      np.round(A.crs_val, 6).tolist()))
+    return "\n".join(parts)

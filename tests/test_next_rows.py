@@ -125,3 +125,37 @@ def test_profile_errors():
     with pytest.raises(report.ProfileError, match="no stage data recorded for cg"):
         report.cg_stage_table(prof)
     assert "stage tables unavailable" in report.format_tables(prof)
+
+
+def test_render_figures_svg_and_csv(tmp_path):
+    # the reference draws PNGs with matplotlib (report.py:179-241); here the
+    # same four figures are SVG plus a CSV of each table
+    import csv
+    import xml.etree.ElementTree as ET
+
+    st = _synthetic_state()
+    prof = report.collect_profile(st)
+    paths = report.render_figures(prof, st.residual_log, tmp_path)
+    names = sorted(p.name for p in paths)
+    assert names == sorted(["residuals.svg", "time_share.svg", "time_share.csv", "cg_stages.svg",
+                            "cg_stages.csv", "assembly_norm.svg", "assembly_norm.csv"])
+    for p in paths:
+        if p.suffix == ".svg":
+            root = ET.parse(p).getroot()
+            assert root.tag.endswith("svg")
+    for stem, fn in (("time_share", report.solver_share_table), ("cg_stage", None),
+                     ("assembly_norm", report.assembly_norm_table)):
+        if fn is None:
+            continue
+        h, rows = fn(prof)
+        with open(tmp_path / f"{stem}.csv") as f:
+            got = list(csv.reader(f))
+        assert tuple(got[0]) == h and len(got) == len(rows) + 1
+        assert [r[0] for r in got[1:]] == [r[0] for r in rows]
+    # the residual chart has one polyline per (solver, field) series
+    svg = (tmp_path / "residuals.svg").read_text()
+    assert svg.count("<polyline") == 4  # ux, uy, uz, p
+    # without stage data only the residual and time-share figures are written
+    st.stage_times = {}
+    paths = report.render_figures(report.collect_profile(st), st.residual_log, tmp_path / "b")
+    assert sorted(p.name for p in paths) == ["residuals.svg", "time_share.csv", "time_share.svg"]
