@@ -411,41 +411,115 @@ def index_bytes_per_row(h, n_rows, K):
     return 1.0 + 4.0 * K * ne.value / max(n_rows, 1), nc.value, df.value
 
 
-def measure_c2(steps, warmup):
-    """BASELINE configs[1] (gen_cavity(128), 1 B200) device-timed, for
-    reference next to the C5 headline (not the bench line's value)."""
+def cg_kernel_roofline(h, kernel_rows, n_rows, K):
+    """Algorithmic bytes and HBM fraction of the persistent CG launches in
+    kernel_rows ((solver, iterations, kernel seconds) per solve): per launch
+    N(12K+80) setup + iterations x N(8K + idx + vec) (idx
+    and vec from the context's format, index_bytes_per_row)."""
+    idx_row, n_codes, defer = index_bytes_per_row(h, n_rows, K)
+    vec = 88 if defer else 96
+    cg = [(it, ks) for sv, it, ks in kernel_rows if sv == "cg"]
+    nbytes = sum(n_rows * (12 * K + 80) + it * n_rows * (8 * K + idx_row + vec) for it, _ in cg)
+    secs = sum(ks for _, ks in cg)
+    peak, _ = peaks()
+    gbs = nbytes / secs / 1e9 if secs > 0 else 0.0
+    return {"k_cg_gbs": gbs, "k_cg_frac": gbs / peak, "k_cg_ms": 1e3 * secs,
+            "bytes_model": f"N(12K+80) + it*N(8K+{idx_row:.3g}+{vec}), K={K}, "
+                           + (f"{n_codes} stencil codes" if n_codes else "explicit int32 indices")}
+
+
+def bicgstab_roofline(kernel_rows, n_rows, K, codes):
+    """k_bicgstab3 algorithmic bytes per batched launch: matrix 2(8K + idx)
+    per row and batched iteration plus 160 B of vectors per row and
+    component-iteration (setup N(12K+56) per component)."""
+    rows = [(it, ks) for sv, it, ks in kernel_rows if sv == "bicgstab"]
+    nbytes = secs = 0.0
+    for j in range(0, len(rows), 3):
+        its = [it for it, _ in rows[j:j + 3]]
+        idx = 1.0 if codes else 4.0 * K
+        nbytes += n_rows * (max(its) * 2 * (8 * K + idx) + 160 * sum(its)
+                            + len(its) * (12 * K + 56))
+        secs += rows[j][1]
+    peak, _ = peaks()
+    gbs = nbytes / secs / 1e9 if secs > 0 else 0.0
+    return {"k_bicgstab_gbs": gbs, "k_bicgstab_frac": gbs / peak, "k_bicgstab_ms": 1e3 * secs}
+
+
+def _timed_steps(st, step, h, steps, warmup):
     import ctypes as C
 
     from paper_1207_1571_b200 import _lib
+
+    for _ in range(warmup):
+        step()
+    rows = []
+    n0 = len(st.residual_log)
+    _lib.check(_lib.lib.fvb_sync(h))
+    _lib.check(_lib.lib.fvb_timer_start(h))
+    for _ in range(steps):
+        step()
+        rows.extend(st._last_solves)
+    ms = C.c_double()
+    _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
+    return ms.value / steps, rows, st.residual_log[n0:]
+
+
+def measure_c2(steps, warmup):
+    """BASELINE configs[1] (gen_cavity(128), 1 B200) device-timed, for
+    reference next to the C5 headline (not the bench line's value)."""
     from paper_1207_1571_b200.coupling import CouplingConfig, init_state, piso_time_step
 
     case = make_case(128)
     cfg = CouplingConfig.from_case_config(case.config)
     st = init_state(case, cfg)
     h = st._ctx.h
-    for _ in range(warmup):
-        piso_time_step(st, cfg)
-    rows = []
-    _lib.check(_lib.lib.fvb_sync(h))
-    _lib.check(_lib.lib.fvb_timer_start(h))
-    for _ in range(steps):
-        piso_time_step(st, cfg)
-        rows.extend(st._last_solves)
-    ms = C.c_double()
-    _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
+    ms_step, rows, _ = _timed_steps(st, lambda: piso_time_step(st, cfg), h, steps, warmup)
     N, K = case.mesh.n_cells, st.pattern.k
-    cg = [(it, ks) for sv, it, ks in rows if sv == "cg"]
-    idx_row, _, defer = index_bytes_per_row(h, N, K)
-    cg_bytes = sum(N * (12 * K + 80) + it * N * (8 * K + idx_row + (88 if defer else 96))
-                   for it, _ in cg)
-    cg_time = sum(ks for _, ks in cg)
-    peak, _ = peaks()
-    ms_step = ms.value / steps
-    return {"workload": "C2 gen_cavity(128) PISO dt=0.1/128, reference defaults",
-            "cells": N, "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
-            "value": N / (ms_step / 1e3), "unit": "cell-updates/s",
-            "k_cg_gbs": cg_bytes / cg_time / 1e9, "k_cg_frac": cg_bytes / cg_time / 1e9 / peak,
-            "cg_iters_per_step": sum(it for it, _ in cg) / steps}
+    out = {"workload": "C2 gen_cavity(128) PISO dt=0.1/128, reference defaults",
+           "cells": N, "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
+           "value": N / (ms_step / 1e3), "unit": "cell-updates/s",
+           "cg_iters_per_step": sum(it for sv, it, _ in rows if sv == "cg") / steps}
+    out.update(cg_kernel_roofline(h, rows, N, K))
+    out.update(bicgstab_roofline(rows, N, K, index_bytes_per_row(h, N, K)[1] > 0))
+    return out
+
+
+def measure_c3(nh, sweeps, warmup, cpu=None):
+    """BASELINE configs[2] (C3: backward-facing step, steady SIMPLE) at the
+    throughput sizes SURVEY.md §8(d) names (nh = 64: 266,240 cells; nh = 128:
+    1,064,960 cells), max_iters raised to 20000 (the 2000 cap binds from
+    nh ~ 32; the same override applies to the reference), device ms per
+    sweep over fixed sweeps after warm-up sweeps from rest, CG kernel
+    roofline.  cpu: the CPU sampler's per-iteration costs (kind, cells,
+    per-iteration seconds) for a labelled reference estimate."""
+    from paper_1207_1571_b200 import cases
+    from paper_1207_1571_b200.coupling import (CouplingConfig, init_state,
+                                               simple_outer_iteration)
+
+    case = cases.gen_backward_step(nh)
+    case.config.max_iters = 20000
+    cfg = CouplingConfig.from_case_config(case.config)
+    st = init_state(case, cfg)
+    h = st._ctx.h
+    ms, rows, log = _timed_steps(st, lambda: simple_outer_iteration(st, cfg), h, sweeps, warmup)
+    N, K = case.mesh.n_cells, st.pattern.k
+    cg = sum(it for sv, it, _ in rows if sv == "cg") / sweeps
+    bi = sum(it for sv, it, _ in rows if sv == "bicgstab") / sweeps
+    out = {"workload": f"C3 gen_backward_step({nh}) SIMPLE, max_iters 20000, sweeps "
+                       f"{warmup + 1}..{warmup + sweeps} from rest",
+           "cells": N, "K": K, "sweeps": sweeps, "warmup": warmup, "ms_per_sweep": ms,
+           "value": N / (ms / 1e3), "unit": "cell-updates/s",
+           "cg_iters_per_sweep": cg, "bicgstab_iters_per_sweep": bi}
+    out.update(cg_kernel_roofline(h, rows, N, K))
+    if cpu is not None:
+        m = CpuSampler.model(cpu["samples"], {"cg": cg, "cg_solves": 1, "bicgstab": bi,
+                                              "bicgstab_solves": 3}, cpu["cells"], N)
+        out["reference_estimate"] = {
+            "ms_per_sweep": 1e3 * m["s_per_step"], "kind": cpu["kind"],
+            "basis": (f"CPU per-iteration and assembly costs measured on gen_cavity("
+                      f"{round(cpu['cells'] ** (1 / 3))}) (cpu_baseline), scaled to this run's "
+                      "iteration counts and cells (an estimate, not a run)")}
+    return out
 
 
 def measure_small():
@@ -487,6 +561,7 @@ def measure_small():
                                   "cg_iters_per_step": st.cum_iters["cg"] / 100,
                                   "reference_ms_per_step_surveyed": 7.4},
             "c3_bfs_nh16": {"ms_per_sweep": 1e3 * c3, "sweeps": 20, "cells": case.mesh.n_cells,
+                            "cg_iters_per_sweep": st3.cum_iters["cg"] / 21,
                             "reference_ms_per_sweep_surveyed": 689.0}}
 
 
@@ -494,7 +569,9 @@ def measure_c4(steps, warmup):
     """BASELINE configs[3] (C4: perturbed + randomly renumbered 126^3 cavity,
     2,000,376 cells, one non-orthogonal corrector): device ms per PISO step.
     The renumbering leaves no stencil codes; the solvers run in their
-    internal RCM order (fvb_pattern_codes reports the solves)."""
+    internal RCM order on explicit indices (fvb_pattern_codes reports the
+    solves); the roofline uses the explicit-index bytes (12K + 88 per row
+    and iteration with the deferred x update)."""
     import ctypes as C
 
     from paper_1207_1571_b200 import _lib, cases
@@ -504,25 +581,20 @@ def measure_c4(steps, warmup):
     cfg = CouplingConfig.from_case_config(case.config)
     st = init_state(case, cfg)
     h = st._ctx.h
-    for _ in range(warmup):
-        piso_time_step(st, cfg)
-    n0 = len(st.residual_log)
     r0, r1 = C.c_int64(), C.c_int64()
     _lib.check(_lib.lib.fvb_pattern_codes(h, None, None, None, C.byref(r0)))
-    _lib.check(_lib.lib.fvb_sync(h))
-    _lib.check(_lib.lib.fvb_timer_start(h))
-    for _ in range(steps):
-        piso_time_step(st, cfg)
-    ms = C.c_double()
-    _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(ms)))
+    ms_step, rows, _ = _timed_steps(st, lambda: piso_time_step(st, cfg), h, steps, warmup)
     _lib.check(_lib.lib.fvb_pattern_codes(h, None, None, None, C.byref(r1)))
-    cg = [r[3] for r in st.residual_log[n0:] if r[0] == "cg"]
-    ms_step = ms.value / steps
-    return {"workload": "C4 perturbed_cavity(126) PISO, randomly renumbered, reference defaults",
-            "cells": case.mesh.n_cells, "steps": steps, "warmup": warmup,
-            "ms_per_step": ms_step, "value": case.mesh.n_cells / (ms_step / 1e3),
-            "unit": "cell-updates/s", "cg_iters_per_step": sum(cg) / steps,
-            "solves_in_rcm_order": r1.value - r0.value}
+    N, K = case.mesh.n_cells, st.pattern.k
+    out = {"workload": "C4 perturbed_cavity(126) PISO, randomly renumbered, reference defaults",
+           "cells": N, "steps": steps, "warmup": warmup,
+           "ms_per_step": ms_step, "value": N / (ms_step / 1e3),
+           "unit": "cell-updates/s",
+           "cg_iters_per_step": sum(it for sv, it, _ in rows if sv == "cg") / steps,
+           "solves_in_rcm_order_incl_warmup": r1.value - r0.value}
+    out.update(cg_kernel_roofline(h, rows, N, K))
+    out.update(bicgstab_roofline(rows, N, K, False))
+    return out
 
 
 def run_ours(args):
@@ -658,12 +730,15 @@ def run_ours(args):
                "measured": meas, "extrapolated": ext}
     # ------------------ auxiliary configs at N=1: C2 (configs[1]), C1/C3
     # (configs[0], [2]) and C4 (configs[3], the renumbered 2M-cell mesh)
-    aux = aux_small = aux_c4 = None
+    aux = aux_small = aux_c4 = aux_c3 = None
     if D.world == 1 and n != 128 and not args.no_aux:
         aux = measure_c2(steps=3, warmup=2)
     if D.world == 1 and not args.no_aux:
         aux_small = measure_small()
         aux_c4 = measure_c4(steps=3, warmup=2)
+        cpu_costs = ({"samples": samples, "cells": s.n, "kind": s.kind} if cpu else None)
+        aux_c3 = {f"nh{nh}": measure_c3(nh, sweeps=2, warmup=3, cpu=cpu_costs)
+                  for nh in (64, 128)}
     out = {
         "metric": METRIC,
         "value": N / (ms_step / 1e3),
@@ -704,6 +779,7 @@ def run_ours(args):
         "cg_iterations_per_launch": [it for it, _ in cg_k],
         "bicgstab_iterations_per_launch": (lambda b: [max(b[i:i + 3]) for i in range(0, len(b), 3)])(
             [it for sv, it, _ in kernel_rows if sv == "bicgstab"]),
+        "bicgstab_roofline": bicgstab_roofline(kernel_rows, n_local, K, n_codes > 0),
         "kernel_ms_per_step": {
             "k_cg": 1e3 * D.max(sum(ks for sv, _, ks in kernel_rows if sv == "cg")) / args.steps,
             # the 3 batched momentum solves share one launch (its time is on each row)
@@ -715,6 +791,7 @@ def run_ours(args):
         "aux_c2_128": aux,
         "aux_small": aux_small,
         "aux_c4_126": aux_c4,
+        "aux_c3": aux_c3,
     }
     if D.rank == 0:
         print(json.dumps(out))

@@ -333,6 +333,12 @@ int fvb_set_sm_share(fvb_ctx* ctx, int share);
 #define FVB_SOLVER_NO_RCM 2         /* solve in the mesh order on renumbered meshes */
 int fvb_set_solver_options(fvb_ctx* ctx, int flags);
 
+/* grid of the persistent solver kernels (no reference counterpart): at most
+ * max_blocks cooperative blocks; 0 = automatic (one block per SM on large
+ * systems, fewer on small ones, where the grid barriers dominate).  Changes
+ * only the grouping of the dot-product partial sums. */
+int fvb_set_solver_grid(fvb_ctx* ctx, int max_blocks);
+
 /* solver data formats of the uploaded pattern (no reference counterpart;
  * bench/roofline evidence): n_codes distinct column-offset tuples of the
  * stencil-code compression (0 = off or FVB_SOLVER_EXPLICIT_INDEX set:

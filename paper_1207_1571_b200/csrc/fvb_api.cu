@@ -262,22 +262,6 @@ __global__ void k_u_corr(int n, size_t nv, const double* hv, const double* rau, 
     for (int c = 0; c < 3; ++c) u[c * nv + i] = hv[c * nv + i] - rau[i] * gp[c * nv + i];
 }
 
-// ||x_c||^2 over the owned rows of the whole team (deterministic)
-int sumsq(Ctx* c, int ncomp, const double* x, double* out) {
-  const int blocks = 2 * c->num_sms;
-  { k_sumsq<<<blocks, kThreads, 0, c->stream>>>(c->nr, size_t(c->nc), ncomp, x, c->partials); fvb::note_launch(); }
-  FVB_CUDA(cudaGetLastError());
-  std::vector<double> h(3 * size_t(blocks));
-  FVB_TRY(d2h(c, h.data(), c->partials, h.size()));
-  FVB_TRY(sync(c));
-  for (int k = 0; k < ncomp; ++k) {
-    double s = 0.0;
-    for (int b = 0; b < blocks; ++b) s += h[size_t(k) * blocks + b];
-    out[k] = s;
-  }
-  return team_allreduce(c, out, ncomp, RED_SUM);
-}
-
 // ----------------------------------------------------------- step state
 // Cell vectors of the step live in pool slots (Slot enum); matrices and
 // face arrays are plain allocations owned by the context.
@@ -407,21 +391,31 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, nv, c->slot(S_B0), c->vol, gp, diag, c->u, rhs,
                                            w.Vm, c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
-  double bn2[3];
-  FVB_TRY(sumsq(c, 3, rhs, bn2));
+  // ||b_c|| of the three solve right-hand sides: block partials on the
+  // device, read back with the solve's results (one host sync for both)
+  const int sblocks = 2 * c->num_sms;
+  double* spart = c->partials + kStepPartials;
+  { k_sumsq<<<sblocks, kThreads, 0, c->stream>>>(c->nr, nv, 3, rhs, spart); fvb::note_launch(); }
+  FVB_CUDA(cudaGetLastError());
+  std::vector<double> hpart(3 * size_t(sblocks));
+  const Readback rb{spart, hpart.data(), 3 * sblocks};
+  FVB_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  const double* b[3] = {rhs, rhs + nv, rhs + 2 * nv};
+  double* x[3] = {c->u, c->u + nv, c->u + 2 * nv};
+  SolveOut out[3];
+  FVB_TRY(bicgstab_solve(c, MatView{w.Vm, w.crsm}, 3, b, x, cfg->mom_tol, cfg->mom_abs_tol,
+                         cfg->mom_max_iters, out, &rb));
+  FVB_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  double bn2[3] = {0.0, 0.0, 0.0};
+  for (int k = 0; k < 3; ++k)
+    for (int q = 0; q < sblocks; ++q) bn2[k] += hpart[size_t(k) * sblocks + q];
+  FVB_TRY(team_allreduce(c, bn2, 3, RED_SUM));
   double bn[3], bscale = 0.0;
   for (int k = 0; k < 3; ++k) {
     bn[k] = std::sqrt(bn2[k]);
     bscale = std::max(bscale, bn[k]);
   }
   bscale = std::max(bscale, 1e-30);
-  FVB_CUDA(cudaEventRecord(c->ev[2], c->stream));
-  const double* b[3] = {rhs, rhs + nv, rhs + 2 * nv};
-  double* x[3] = {c->u, c->u + nv, c->u + 2 * nv};
-  SolveOut out[3];
-  FVB_TRY(bicgstab_solve(c, MatView{w.Vm, w.crsm}, 3, b, x, cfg->mom_tol, cfg->mom_abs_tol,
-                         cfg->mom_max_iters, out));
-  FVB_CUDA(cudaEventRecord(c->ev[3], c->stream));
   static const char* names[3] = {"ux", "uy", "uz"};
   double worst = 0.0;
   for (int k = 0; k < 3; ++k) {
@@ -445,7 +439,8 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
 
 // _pressure_correct (coupling.py:282-344)
 int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_report* rep,
-                     double* first_res, double* t_asm, double* t_solve, double* t_corr) {
+                     double* first_res, double* t_asm, double* t_solve, double* t_corr,
+                     int corr_index) {
   StepWork w = work_of(c);
   const int n = c->nr;
   const size_t nv = c->nc;
@@ -510,7 +505,12 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
     if (*first_res < 0) *first_res = o.res0;
     FVB_TRY(team_halo(c, S_P, 1));  // unrelaxed p on processor faces
   }
-  FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
+  // the correction tail is timed by an event pair read at the end of the
+  // step (no host sync here: the next corrector's launches queue behind it)
+  const bool defer = corr_index < Ctx::kTailPairs;
+  cudaEvent_t e0 = defer ? c->cev[2 * corr_index] : c->ev[6];
+  cudaEvent_t e1 = defer ? c->cev[2 * corr_index + 1] : c->ev[7];
+  FVB_CUDA(cudaEventRecord(e0, c->stream));
   FVB_TRY(op_lap_flux(c, 1, 1, w.coef, w.corr, c->p, c->pb, w.lf));
   { k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux); fvb::note_launch(); }
   if (relax_p && cfg->alpha_p < 1.0) {
@@ -529,11 +529,17 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
   FVB_CUDA(cudaGetLastError());
   FVB_TRY(team_halo(c, S_U, 3));
   FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
-  FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
-  FVB_CUDA(cudaEventSynchronize(c->ev[7]));
-  *t_asm += (ev_ms(c, 4, 5) + asm_ms) * 1e-3;
+  FVB_CUDA(cudaEventRecord(e1, c->stream));
+  *t_asm += (ev_ms(c, 4, 5) + asm_ms) * 1e-3;  // complete: the CG readback synced
   *t_solve += solve_ms * 1e-3;
-  *t_corr += ev_ms(c, 6, 7) * 1e-3;
+  if (defer) {
+    c->n_tail = corr_index + 1;
+  } else {
+    FVB_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FVB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *t_corr += ms * 1e-3;
+  }
   return FVB_OK;
 }
 
@@ -563,11 +569,17 @@ int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_rep
   rep->t_momentum_solve = ev_ms(c, 2, 3) * 1e-3;
   double first = -1.0;
   const int ncorr = piso ? cfg->n_correctors : 1;
+  c->n_tail = 0;
   for (int k = 0; k < ncorr; ++k)
     FVB_TRY(pressure_correct(c, cfg, !piso, rep, &first, &rep->t_pressure_assembly,
-                             &rep->t_pressure_solve, &rep->t_correction));
+                             &rep->t_pressure_solve, &rep->t_correction, k));
   rep->p_res = first;
   FVB_CUDA(cudaStreamSynchronize(c->stream));
+  for (int k = 0; k < c->n_tail; ++k) {
+    float ms = 0.f;
+    FVB_CUDA(cudaEventElapsedTime(&ms, c->cev[2 * k], c->cev[2 * k + 1]));
+    rep->t_correction += ms * 1e-3;
+  }
   op_collect(c, rep);
   if (c->teamed()) {
     unsigned err = 0;
@@ -611,6 +623,7 @@ int fvb_ctx_create(int device, fvb_ctx** out) {
   for (auto& ev : c->tev) cudaEventCreate(&ev);
   for (auto& ev : c->kev) cudaEventCreate(&ev);
   for (auto& ev : c->opev) cudaEventCreate(&ev);
+  for (auto& ev : c->cev) cudaEventCreate(&ev);
   int rc = dalloc(c, &c->sync, 64);
   if (!rc) rc = dalloc(c, &c->partials, 16 * 4096 + 256);
   if (!rc) rc = dalloc(c, &c->ipart, 64);
@@ -636,6 +649,8 @@ int fvb_ctx_destroy(fvb_ctx* h) {
   for (auto& ev : c->kev)
     if (ev) cudaEventDestroy(ev);
   for (auto& ev : c->opev)
+    if (ev) cudaEventDestroy(ev);
+  for (auto& ev : c->cev)
     if (ev) cudaEventDestroy(ev);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete h;
@@ -1560,6 +1575,15 @@ int fvb_set_solver_options(fvb_ctx* h, int flags) {
     return FVB_E_ARG;
   }
   h->c.solver_flags = flags;
+  return FVB_OK;
+}
+
+int fvb_set_solver_grid(fvb_ctx* h, int max_blocks) {
+  if (max_blocks < 0) {
+    fvb_set_error("max_blocks %d < 0", max_blocks);
+    return FVB_E_ARG;
+  }
+  h->c.solver_max_blocks = max_blocks;
   return FVB_OK;
 }
 

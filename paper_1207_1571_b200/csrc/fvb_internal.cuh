@@ -187,9 +187,14 @@ struct Ctx {
   int num_sms = 148;
   int sm_share = 1;                 // teams sharing one device (tests): grid / sm_share
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev[8];
+  cudaEvent_t ev[8] = {};
   cudaEvent_t tev[2];
   cudaEvent_t kev[2];
+  // correction-tail event pairs of one step's correctors, read after the
+  // step's final sync (pressure_correct)
+  static constexpr int kTailPairs = 8;
+  cudaEvent_t cev[2 * kTailPairs] = {};
+  int n_tail = 0;
   // per-operator timing of one step (RunState.ops): event pairs + op ids
   static constexpr int kOpEvents = 96;
   cudaEvent_t opev[kOpEvents];
@@ -224,6 +229,7 @@ struct Ctx {
   double* rcm_vec = nullptr;  // BiCGStab: b', x' per component + 1/D'
   int64_t cg_rcm_solves = 0;
   int solver_flags = 0;      // FVB_SOLVER_* (fvb_set_solver_options)
+  int solver_max_blocks = 0; // persistent solver grid cap (fvb_set_solver_grid; 0 = auto)
   int64_t bi_rcm_solves = 0;
   int *crs_ptr = nullptr, *crs_col = nullptr, *crs_face = nullptr;
   // boundary conditions: 0 = u (3 comps), 1 = p
@@ -292,6 +298,12 @@ int dalloc(Ctx* c, T** out, size_t n) {
 
 // create the cell pool once nc is known (mesh or pattern upload)
 int ensure_pool(Ctx* c);
+
+// Regions of Ctx::partials (16*4096 + 256 doubles): grid-reduction partials
+// from 0 (at most 2 x 9 x 2 x 148 doubles), step-level block partials read
+// back with a solve's results, solver results, team allreduce staging.
+constexpr size_t kStepPartials = 32768;
+constexpr size_t kResults = 16 * 4096;
 
 // ------------------------------------------------------- kernel helpers
 inline int grid_for(int64_t n, int threads, int cap = 148 * 32) {
@@ -493,14 +505,26 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // broadcast through the sync area.  sync words: [0] arrivals, [1]
 // generation, [2] abort flag, [4..) broadcast doubles.  The barrier also
 // orders every halo store issued before it.  Returns false on watchdog.
+// Partials of consecutive reductions alternate between two buffers of
+// kRedStride x gridDim.x doubles.  The buffer stride must not depend on M:
+// with a stride of M x gridDim.x, a fast block writing the partials of
+// reduction k+1 (M = 2) overlapped the upper half of reduction k's buffer
+// (M = 1) while a slow block could still be reading it — a rare wrong
+// p.q in one block (profiles/r02_stress.md).
+constexpr size_t kRedStride = 16;
+
 template <int M, bool OOL = false>
 __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
                                             double* smem /*[32*M+M]*/, unsigned& rnd,
                                             bool sends = true) {
+  static_assert(M <= int(kRedStride), "team_reduce: at most kRedStride values");
   __shared__ int s_last, s_ok;
   __shared__ unsigned s_gen;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef FVB_DIAG_FENCE  // diagnostic build (tools/build_variant.py): every thread fences
+  __threadfence();
+#endif
   if (T.size <= 1) {
     // One device: a monotonic arrival counter, no last-arriver hand-off.
     // Every block publishes its partials, arrives with a release add and
@@ -525,7 +549,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
       return true;
     }
     const unsigned r = rnd++;
-    double* part = partials + size_t(r & 1u) * size_t(M) * gridDim.x;
+    double* part = partials + size_t(r & 1u) * kRedStride * gridDim.x;
     volatile unsigned* vabort = sync + 2;
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -542,7 +566,13 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
           break;
         }
       }
-      ld_acquire_gpu(sync);  // acquire (+ L1 invalidate) before reading results
+      // acquire before anyone reads partials or vectors of other blocks.
+      // The load's value must be used: ptxas drops an ld.acquire whose
+      // result is discarded and keeps only its L1 invalidate, which left
+      // the relaxed polls above as the only synchronisation — a 1-in-100
+      // run-to-run difference in the 128^3 stress (profiles/r02_stress.md).
+      while (ld_acquire_gpu(sync) < target && *vabort == 0) {
+      }
       s_ok = *vabort == 0;
     }
     __syncthreads();
@@ -561,6 +591,9 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
     const bool ok = s_ok != 0;
     __syncthreads();
+#ifdef FVB_DIAG_FENCE
+    __threadfence();
+#endif
     return ok;
   }
   // teamed: the result goes through the peer mailboxes (broadcast path);
@@ -585,14 +618,14 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     // partials double-buffered by generation parity: a block can only write
     // the partial of reduction k+2 after every block passed reduction k+1,
     // i.e. after every block finished reading the partials of reduction k
-    double* part = partials + size_t(gen & 1u) * size_t(M) * gridDim.x;
+    double* part = partials + size_t(gen & 1u) * kRedStride * gridDim.x;
 #pragma unroll
     for (int m = 0; m < M; ++m) part[size_t(m) * gridDim.x + blockIdx.x] = v[m];
     s_last = atom_arrive(sync, sys) == gridDim.x - 1;
   }
   __syncthreads();
   const unsigned gen = s_gen;
-  const double* part = partials + size_t(gen & 1u) * size_t(M) * gridDim.x;
+  const double* part = partials + size_t(gen & 1u) * kRedStride * gridDim.x;
   if (s_last) {
     if (!teamed) {
       if (threadIdx.x == 0) {
@@ -632,7 +665,9 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     }
   }
   if (threadIdx.x == 0) {
-    ld_acquire_gpu(sync + 1);  // acquire (+ L1 invalidate) before reading results
+    // acquire (value used, see the single-device path) before reading results
+    while (ld_acquire_gpu(sync + 1) == gen && *vabort == 0) {
+    }
     s_ok = *vabort == 0;
     if (teamed) {
 #pragma unroll
@@ -684,9 +719,16 @@ enum SolveErr {
   SE_OMEGA = 6,
   SE_TIMEOUT = 7,
 };
+// Extra device -> host copy folded into a solve's result readback (one
+// stream sync for both).
+struct Readback {
+  const double* dev;
+  double* host;
+  int n;
+};
 // x must hold x0 on entry (ghost entries current); returns solution in x.
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol,
-             double abs_tol, int max_iters, SolveOut* out);
+             double abs_tol, int max_iters, SolveOut* out, const Readback* extra = nullptr);
 // true when cg_solve folds x += alpha p into the next pass A (7-point rows)
 bool cg_defers_x(const Ctx* c);
 // the solvers read stencil codes / run in RCM order (format options)
@@ -694,7 +736,7 @@ bool uses_codes(const Ctx* c);
 bool uses_rcm(const Ctx* c);
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
                    double* const* x, double tol, double abs_tol, int max_iters,
-                   SolveOut* out);
+                   SolveOut* out, const Readback* extra = nullptr);
 std::string solve_error_text(const char* solver, const SolveOut& o, int zero_row);
 
 // team collectives (fvb_team.cu): halo exchange of consecutive pool slots

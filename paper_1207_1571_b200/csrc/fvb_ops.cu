@@ -406,7 +406,8 @@ __global__ void k_inv_diag(int n, const int* __restrict__ ds, const double* __re
                            double* __restrict__ inv, int* first_zero) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const double d = V[size_t(ds[i]) * n + i];
-    if (d == 0.0) atomicMin(first_zero, i);
+    // first zero-diagonal row, encoded INT_MAX - row (0 = none; max = first)
+    if (d == 0.0) atomicMax(first_zero, 0x7fffffff - i);
     inv[i] = 1.0 / d;
   }
 }

@@ -48,7 +48,25 @@ struct CgParams {
   unsigned* sync;
   double* partials;
   double* result;  // [iters, converged, res0, res, err_kind, err_iter]
+  const int* zero_flag;  // single domain: k_inv_diag's first zero row (INT_MAX - row), or null
 };
+
+// A zero diagonal (found by the k_inv_diag launch before the solve) ends
+// the solve before its first pass, with the reference's error and row; every
+// block reads the same flag, so no block enters a barrier alone.
+__device__ __forceinline__ bool zero_diag_exit(const int* flag, double* result, int ncomp) {
+  if (!flag) return false;
+  const int v = *flag;
+  if (v == 0) return false;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int c = 0; c < ncomp; ++c)
+      for (int k = 0; k < 6; ++k) result[6 * c + k] = 0.0;
+    result[4] = SE_ZERO_DIAG;
+    result[5] = double(0x7fffffff - v);
+    for (int k = 6 * ncomp; k < 6 * ncomp + 3; ++k) result[k] = 0.0;
+  }
+  return true;
+}
 
 // Pass A with the column indices (the gather's address chain) prefetched
 // DEPTH rows ahead; the values V of the current row are loaded in-iteration
@@ -153,7 +171,11 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
     const int r = i + d * step;
     cq[d] = r < end ? int(__ldcs(code + r)) : 0;
   }
+#ifdef FVB_DIAG_GATHER_CG  // diagnostic build: gathers bypass L1
+  auto g = [&](int col) { return first ? __ldcg(z + col) : __ldcg(po + col) * beta + __ldcg(z + col); };
+#else
   auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
+#endif
   while (i < end) {
     double vi[KT];
 #pragma unroll
@@ -217,6 +239,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     for (int j = threadIdx.x; j < A.P.ncode * KT; j += blockDim.x) s_tab[j] = A.P.stab[j];
     __syncthreads();
   }
+  if (zero_diag_exit(A.zero_flag, A.result, 1)) return;
   constexpr bool PB2 = KT > 0;
   const PatternView& P = A.P;
   const TeamView& T = A.T;
@@ -553,6 +576,7 @@ struct Bi3Params {
   unsigned* sync;
   double* partials;
   double* result;
+  const int* zero_flag;  // as CgParams::zero_flag
 };
 
 template <int KT, int NC, bool SC = false>
@@ -564,6 +588,10 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
   if (SC) {
     for (int j = threadIdx.x; j < A.P.ncode * KT; j += blockDim.x) s_tab[j] = A.P.stab[j];
     __syncthreads();
+  }
+  if (zero_diag_exit(A.zero_flag, A.result, NC)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.result[18] = A.result[19] = A.result[20] = 0.0;
+    return;
   }
   const PatternView& P = A.P;
   const TeamView& T = A.T;
@@ -922,6 +950,8 @@ int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   // small systems: one block (block barriers instead of grid barriers) while
   // the rows per thread stay low
   if (!c->teamed() && c->nr <= 4 * threads) b = 1;
+  if (c->solver_max_blocks > 0 && b > c->solver_max_blocks) b = c->solver_max_blocks;
+  if (b > int(kStepPartials / (2 * kRedStride))) b = int(kStepPartials / (2 * kRedStride));
   *blocks = b < 1 ? 1 : b;
   return FVB_OK;
 }
@@ -947,19 +977,24 @@ int coop_launch(Ctx* c, K kernel, Args& args, int threads = kSolverThreads, int 
   return FVB_OK;
 }
 
-// inverse diagonal of the owned rows; a zero diagonal anywhere in the team
-// is reported on every rank (so no rank enters the solve alone)
-int check_zero_diag(Ctx* c, MatView A, double* inv, int* zero_row) {
+// Inverse diagonal of the owned rows, and the first zero-diagonal row into
+// c->ipart[0] (INT_MAX - row; 0 = none).  A team reads it back now, so a zero
+// diagonal anywhere is reported on every rank before any rank enters the
+// solve; a single domain leaves it to the solver kernel (zero_diag_exit), so
+// the solve needs no host round trip before its launch.  zero_row: INT_MAX,
+// or the row when the team found one.
+int prepare_diag(Ctx* c, MatView A, double* inv, int* zero_row) {
   int* dz = c->ipart;
-  const int big = 0x7fffffff;
-  FVB_CUDA(cudaMemcpyAsync(dz, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  *zero_row = 0x7fffffff;
+  FVB_CUDA(cudaMemsetAsync(dz, 0, sizeof(int), c->stream));
   FVB_TRY(launch_inv_diag(c, A.V, inv, dz));
-  FVB_CUDA(cudaMemcpyAsync(zero_row, dz, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  FVB_CUDA(cudaStreamSynchronize(c->stream));
   if (c->teamed()) {
-    double v = double(*zero_row);
-    FVB_TRY(team_allreduce(c, &v, 1, RED_MIN));
-    *zero_row = int(v);
+    int v = 0;
+    FVB_CUDA(cudaMemcpyAsync(&v, dz, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    FVB_CUDA(cudaStreamSynchronize(c->stream));
+    double m = double(v ? 0x7fffffff - v : 0x7fffffff);
+    FVB_TRY(team_allreduce(c, &m, 1, RED_MIN));
+    *zero_row = int(m);
   }
   return FVB_OK;
 }
@@ -1063,7 +1098,7 @@ bool uses_rcm(const Ctx* c) {
 bool cg_defers_x(const Ctx* c) { return c->k == 7; }
 
 int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double abs_tol,
-             int max_iters, SolveOut* out) {
+             int max_iters, SolveOut* out, const Readback* extra) {
   double* inv = c->slot(S_SCR + 0);
   double* r = c->slot(S_SCR + 1);
   double* z = c->slot(S_SCR + 2);
@@ -1072,7 +1107,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   double* q = c->slot(S_SCR + 5);
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
-  FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
+  FVB_TRY(prepare_diag(c, A, inv, &zero_row));
   *out = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (zero_row != 0x7fffffff) {
     out->error_kind = SE_ZERO_DIAG;
@@ -1081,7 +1116,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   }
   CgParams prm{c->pattern(), c->team, A.V, A.crs, inv, b, x, r, z, pa, pb, q,
                S_SCR + 2, S_SCR + 3, S_SCR + 4, tol, abs_tol, max_iters,
-               c->sync, c->partials, result};
+               c->sync, c->partials, result, c->teamed() ? nullptr : c->ipart};
   // RCM order (patterns without stencil codes, one domain, 7-point rows):
   // the solve runs on a permuted copy of the system
   const bool rcm = uses_rcm(c);
@@ -1133,6 +1168,9 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   double h[9];
   unsigned team_err = 0;
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+  if (extra && extra->n)
+    FVB_CUDA(cudaMemcpyAsync(extra->host, extra->dev, sizeof(double) * extra->n,
+                             cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaMemcpyAsync(&team_err, c->sync + 3, sizeof team_err, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
   if (team_err) h[4] = SE_TIMEOUT;
@@ -1183,6 +1221,7 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   prm.sync = c->sync;
   prm.partials = c->partials;
   prm.result = result;
+  prm.zero_flag = c->teamed() ? nullptr : c->ipart;
   // stencil-coded SpMV sweeps when the pattern has codes (unless the
   // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX)
   const bool sc = uses_codes(c);
@@ -1196,11 +1235,12 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
 }
 
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double* const* x,
-                   double tol, double abs_tol, int max_iters, SolveOut* out) {
+                   double tol, double abs_tol, int max_iters, SolveOut* out,
+                   const Readback* extra) {
   double* inv = c->slot(S_SCR + 0);
   double* result = c->partials + 16 * 4096;
   int zero_row = 0x7fffffff;
-  FVB_TRY(check_zero_diag(c, A, inv, &zero_row));
+  FVB_TRY(prepare_diag(c, A, inv, &zero_row));
   for (int k = 0; k < ncomp; ++k) out[k] = SolveOut{0, 0, SE_NONE, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   if (zero_row != 0x7fffffff) {
     out[0].error_kind = SE_ZERO_DIAG;
@@ -1253,6 +1293,9 @@ int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b, double*
   double h[21];
   unsigned team_err = 0;
   FVB_CUDA(cudaMemcpyAsync(h, result, sizeof(double) * 21, cudaMemcpyDeviceToHost, c->stream));
+  if (extra && extra->n)
+    FVB_CUDA(cudaMemcpyAsync(extra->host, extra->dev, sizeof(double) * extra->n,
+                             cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaMemcpyAsync(&team_err, c->sync + 3, sizeof team_err, cudaMemcpyDeviceToHost, c->stream));
   FVB_CUDA(cudaStreamSynchronize(c->stream));
   if (team_err)

@@ -1,0 +1,147 @@
+"""Parity at the BASELINE configurations' NAMED sizes against the real
+reference (fixtures tests/golden/full_*.npz, made by oracle/make_golden_full.py
+from /root/reference's own run_case / piso_time_step).
+
+* C2 gen_cavity(128), PISO steps 1-2: fields (u, p, phi on a seeded
+  32768-cell / 32768-face sample, plus full-field norms) within 1e-8
+  relative L2 at cg_tol 1e-13 / bicgstab_tol 1e-10 (SURVEY.md §7 hard part
+  1 protocol (i)); iteration counts at the reference defaults, CG +-1 and
+  BiCGStab +-2 per solve (protocol (ii)).
+* C3 backward-facing step nh = 16 (16,640 cells), SIMPLE run to convergence
+  by run_case: number of sweeps, converged fields, continuity; per-solve
+  counts over the first sweeps (uz of the one-cell-thick mesh excluded, as
+  SURVEY.md §7 prescribes: its rhs is round-off).
+* C4 perturbed + randomly renumbered 126^3 cavity (2,000,376 cells; the
+  device solvers run in RCM order), one PISO step: fields at tight
+  tolerances, counts at defaults.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import rel
+from paper_1207_1571_b200 import cases
+from paper_1207_1571_b200.coupling import (CouplingConfig, continuity_error, init_state,
+                                           piso_time_step, run_case)
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+FIELD_TOL = 1e-8
+TIGHT = dict(cg_tol=1e-13, bicgstab_tol=1e-10, max_iters=20000)
+
+
+def _gold(name):
+    return np.load(os.path.join(GOLD, f"full_{name}.npz"))
+
+
+def _log_rows(names, log):
+    return [(str(nm).split(":")[0], str(nm).split(":")[1], int(r[0]), int(r[1]))
+            for nm, r in zip(names, log)]
+
+
+def _check_counts(mine, ref, skip_uz=False):
+    """CG +-1, BiCGStab +-2 per solve, same solve sequence."""
+    assert [(a[0], a[1], a[2]) for a in mine] == [(b[0], b[1], b[2]) for b in ref]
+    bad = [(a, b) for a, b in zip(mine, ref)
+           if not (skip_uz and a[1] == "uz") and abs(a[3] - b[3]) > (1 if a[0] == "cg" else 2)]
+    assert not bad, bad
+
+
+def _cavity(n, tight):
+    case = cases.gen_cavity(n)
+    case.config.algorithm, case.config.dt = "piso", 0.1 / n
+    if tight:
+        for k, v in TIGHT.items():
+            setattr(case.config, k, v)
+    return case
+
+
+def _steps(case, g):
+    cfg = CouplingConfig.from_case_config(case.config)
+    st = init_state(case, cfg)
+    ci, fi = g["sample_cells"], g["sample_faces"]
+    out = []
+    for s in range(int(g["steps"])):
+        n0 = len(st.residual_log)
+        piso_time_step(st, cfg)
+        u, p, f = st.u.values, st.p.values, st.flux
+        err = {"u": rel(u[ci], g[f"s{s}_u"]), "p": rel(p[ci], g[f"s{s}_p"]),
+               "flux": rel(f[fi], g[f"s{s}_flux"]),
+               "norm_u": float(np.max(np.abs(np.linalg.norm(u, axis=0) / g[f"s{s}_norm_u"] - 1))),
+               "norm_p": abs(np.linalg.norm(p) / float(g[f"s{s}_norm_p"]) - 1),
+               "norm_flux": abs(np.linalg.norm(f) / float(g[f"s{s}_norm_flux"]) - 1)}
+        rows = [(r[0], r[1], 0, r[3]) for r in st.residual_log[n0:]]
+        ref = [(a, b, 0, n) for a, b, _, n in _log_rows(g[f"s{s}_log_names"], g[f"s{s}_log"])]
+        out.append((err, rows, ref, continuity_error(st), np.abs(f).max()))
+    return out
+
+
+def _fields_ok(results):
+    for s, (err, _rows, _ref, cont, fmax) in enumerate(results):
+        assert max(err.values()) < FIELD_TOL, (s, err)
+        assert cont <= 1e-8 * fmax
+
+
+@pytest.mark.slow
+def test_c2_cavity128_fields_tight_tolerances():
+    g = _gold("c2_tight")
+    res = _steps(_cavity(128, True), g)
+    _fields_ok(res)
+    for _err, rows, ref, _c, _m in res:
+        # counts at tightened tolerances follow the dot-product rounding
+        # (BiCGStab +-3 between two CPU orderings at 64^3)
+        for a, b in zip(rows, ref):
+            assert abs(a[3] - b[3]) <= (2 if a[0] == "cg" else max(3, b[3] // 10)), (a, b)
+
+
+@pytest.mark.slow
+def test_c2_cavity128_iteration_counts_defaults():
+    g = _gold("c2_default")
+    for _err, rows, ref, cont, fmax in _steps(_cavity(128, False), g):
+        _check_counts(rows, ref)
+        assert cont <= 1e-8 * fmax
+
+
+def _c4(tight):
+    case = cases.perturbed_cavity(126)
+    if tight:
+        for k, v in TIGHT.items():
+            setattr(case.config, k, v)
+    return case
+
+
+@pytest.mark.slow
+def test_c4_perturbed_126_fields_tight_tolerances_rcm():
+    g = _gold("c4_tight")
+    res = _steps(_c4(True), g)
+    _fields_ok(res)
+
+
+@pytest.mark.slow
+def test_c4_perturbed_126_iteration_counts_defaults_rcm():
+    g = _gold("c4_default")
+    for _err, rows, ref, cont, fmax in _steps(_c4(False), g):
+        _check_counts(rows, ref)
+        assert cont <= 1e-8 * fmax
+
+
+def test_c3_backward_step_nh16_simple_to_convergence():
+    g = _gold("c3_nh16")
+    case = cases.gen_backward_step(16)
+    st = run_case(case)
+    assert st.converged and bool(g["converged"])
+    ref = _log_rows(g["log_names"], g["log"])
+    mine = [(r[0], r[1], r[2], r[3]) for r in st.residual_log]
+    # the first sweeps solve identical systems up to rounding: counts per
+    # solve within the parity rule (uz of the one-cell-thick mesh excluded)
+    n_early = 4 * 20
+    _check_counts(mine[:n_early], ref[:n_early], skip_uz=True)
+    # the converged state: same number of sweeps to outer_tol, fields within
+    # the field tolerance, continuity at the reference's level
+    assert abs(st.outer - int(g["sweeps"])) <= 1, (st.outer, int(g["sweeps"]))
+    errs = {"u": rel(st.u.values[:, :2], g["u"][:, :2]), "p": rel(st.p.values, g["p"]),
+            "flux": rel(st.flux, g["flux"])}
+    assert max(errs.values()) < FIELD_TOL, errs
+    assert continuity_error(st) <= 1e-8 * np.abs(st.flux).max()

@@ -8,6 +8,8 @@ makes the SpMV sweeps read int32 indices instead of stencil codes
 (fvb_set_solver_options)."""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+if os.environ.get("FVB_PKG_ROOT"):  # A/B of diagnostic builds (tools/build_variant.py)
+    sys.path.insert(0, os.environ["FVB_PKG_ROOT"])
 import numpy as np
 from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for

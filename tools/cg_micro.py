@@ -8,6 +8,8 @@ and "norcm" set the context's solver format options (fvb_set_solver_options:
 explicit int32 indices instead of stencil codes / mesh order instead of RCM)."""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+if os.environ.get("FVB_PKG_ROOT"):  # A/B of diagnostic builds (tools/build_variant.py)
+    sys.path.insert(0, os.environ["FVB_PKG_ROOT"])
 import numpy as np
 from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
@@ -44,6 +46,9 @@ b = np.random.default_rng(0).normal(size=N)
 x = np.empty(N)
 ctx = context_for(None, None, pat)
 _lib.check(_lib.lib.fvb_set_solver_options(ctx.h, opts))
+grid = [int(a[5:]) for a in sys.argv[3:] if a.startswith("grid=")]
+if grid:
+    _lib.check(_lib.lib.fvb_set_solver_grid(ctx.h, grid[0]))
 rep = _lib.SolveReportC()
 P = _lib.ptr
 crs = np.full(max(pat.nnz_crs, 1), -1.0)
@@ -65,7 +70,7 @@ use_codes = codes.value > 0
 # deferred x update (large systems): pass B no longer re-reads p
 bytes_it = N * ((8 * K + 1 if use_codes else 12 * K) + (88 if defer.value else 96))
 setup_b = N * (12 * K + 80)
-print(json.dumps({"options": opts, "n": n, "iters": rep.iterations,
+print(json.dumps({"options": opts, "grid": grid[0] if grid else 0, "n": n, "iters": rep.iterations,
                   "us_per_iter": 1e6 * t / iters,
                   "us_passA": 1e6 * ta / iters, "us_passB": 1e6 * tb / iters,
                   "us_reduce2x": 1e6 * tr / iters,

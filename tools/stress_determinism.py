@@ -26,6 +26,8 @@ import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
+if os.environ.get("FVB_PKG_ROOT"):  # A/B of diagnostic builds (tools/build_variant.py)
+    sys.path.insert(0, os.environ["FVB_PKG_ROOT"])
 
 from paper_1207_1571_b200 import cases  # noqa: E402
 from paper_1207_1571_b200.coupling import (CouplingConfig, continuity_error,  # noqa: E402
@@ -61,6 +63,8 @@ def main():
     ap.add_argument("--reseed", type=int, default=200)
     ap.add_argument("--big", type=int, default=256)
     ap.add_argument("--out", default="profiles/r02_stress.jsonl")
+    ap.add_argument("--step2", type=int, default=0,
+                    help="R repeats of PISO step 2 alone from the saved step-1 state")
     a = ap.parse_args()
     out = open(a.out, "w")
     fails = []
@@ -72,6 +76,32 @@ def main():
         out.flush()
 
     case, cfg = cavity(a.edge)
+    if a.step2:
+        st = init_state(case, cfg)
+        piso_time_step(st, cfg)
+        s1 = (st.u.values.copy(), st.p.values.copy(), st.flux.copy(), st.u.boundary.copy(),
+              st.p.boundary.copy(), st.outer, st.t)
+        ref = None
+        t0 = time.time()
+        for i in range(a.step2):
+            st.u.values, st.p.values, st.flux = s1[0], s1[1], s1[2]
+            st.u.boundary, st.p.boundary = s1[3], s1[4]
+            st.outer, st.t = s1[5], s1[6]
+            n0 = len(st.residual_log)
+            piso_time_step(st, cfg)
+            log = [list(r[:4]) + [float(r[4]).hex(), float(r[5]).hex()]
+                   for r in st.residual_log[n0:]]
+            dg = digest(st)
+            emit("step2", i, log, dg)
+            if ref is None:
+                ref = (log, dg)
+            elif (log, dg) != ref:
+                fails.append(("step2", i))
+                print(f"  step2 {i}: MISMATCH {[r[3] for r in log]}", flush=True)
+        print(f"step2 x{a.step2}: {time.time() - t0:.1f} s, mismatches {len(fails)}", flush=True)
+        out.write(json.dumps({"summary": True, "step2": a.step2, "mismatches": fails}) + "\n")
+        out.close()
+        sys.exit(1 if fails else 0)
     t0 = time.time()
     st = init_state(case, cfg)
     u0, p0, f0 = st.u.values.copy(), st.p.values.copy(), st.flux.copy()
