@@ -649,6 +649,9 @@ def run_ours(args):
     launches = int(_lib.lib.fvb_launch_count() - l0)
     clk = clocks.stop() if clocks else None
     ms_step = D.max(ms.value) / args.steps
+    ranks = None
+    if D.world > 1:  # per-rank evidence (device, peer access, IPC, device ms)
+        ranks = D.allgather(dict(run.diag, ms_per_step=ms.value / args.steps))
     rows = log[nlog:]
     cg_iters = [r[3] for r in rows if r[0] == "cg"]
     bi_iters = [r[3] for r in rows if r[0] == "bicgstab"]
@@ -792,6 +795,7 @@ def run_ours(args):
         "aux_small": aux_small,
         "aux_c4_126": aux_c4,
         "aux_c3": aux_c3,
+        "ranks": ranks,
     }
     if D.rank == 0:
         print(json.dumps(out))

@@ -53,6 +53,9 @@ typedef struct fvb_ctx fvb_ctx;
 
 int fvb_version(void);
 const char* fvb_last_error(void);
+/* cudaDeviceCanAccessPeer (bench/team diagnostics: every rank of a
+ * multi-GPU team stores into its peers' pools over NVLink). */
+int fvb_device_can_access_peer(int device, int peer, int* ok);
 int fvb_device_count(void);
 
 /* ------------------------------------------------------------------ setup

@@ -286,6 +286,7 @@ int ensure_work(Ctx* c) {
   FVB_TRY(dalloc(c, &c->coef, nf));
   FVB_TRY(dalloc(c, &c->corr, nf));
   FVB_TRY(dalloc(c, &c->lf, nf));
+  FVB_TRY(dalloc(c, &c->u_save, 3 * size_t(c->nc)));
   c->work_ready = true;
   return FVB_OK;
 }
@@ -403,6 +404,11 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   const double* b[3] = {rhs, rhs + nv, rhs + 2 * nv};
   double* x[3] = {c->u, c->u + nv, c->u + 2 * nv};
   SolveOut out[3];
+  // the batched solve updates the three components in place; the reference
+  // solves them one by one and raises before assigning a failed one
+  // (coupling.py:259-277), so keep u to restore the unsolved components
+  FVB_CUDA(cudaMemcpyAsync(c->u_save, c->u, sizeof(double) * 3 * nv, cudaMemcpyDeviceToDevice,
+                           c->stream));
   FVB_TRY(bicgstab_solve(c, MatView{w.Vm, w.crsm}, 3, b, x, cfg->mom_tol, cfg->mom_abs_tol,
                          cfg->mom_max_iters, out, &rb));
   FVB_CUDA(cudaEventRecord(c->ev[3], c->stream));
@@ -421,6 +427,9 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   for (int k = 0; k < 3; ++k) {
     if (out[k].error_kind != SE_NONE) {
       rep->failed_solve = rep->n_solves;
+      FVB_CUDA(cudaMemcpyAsync(c->u + k * nv, c->u_save + k * nv, sizeof(double) * (3 - k) * nv,
+                               cudaMemcpyDeviceToDevice, c->stream));
+      FVB_CUDA(cudaStreamSynchronize(c->stream));
       std::string msg = solve_error_text("bicgstab", out[k], out[k].error_iteration);
       fvb_set_error("momentum solve for %s failed at outer {outer}: %s", names[k], msg.c_str());
       return out[k].error_kind == SE_TIMEOUT ? FVB_E_TIMEOUT : FVB_E_COUPLING;
@@ -597,6 +606,16 @@ extern "C" {
 
 int fvb_version(void) { return 100; }
 const char* fvb_last_error(void) { return g_last_error.c_str(); }
+int fvb_device_can_access_peer(int device, int peer, int* ok) {
+  *ok = 0;
+  if (device == peer) {
+    *ok = 1;
+    return FVB_OK;
+  }
+  FVB_CUDA(cudaDeviceCanAccessPeer(ok, device, peer));
+  return FVB_OK;
+}
+
 int fvb_device_count(void) {
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;

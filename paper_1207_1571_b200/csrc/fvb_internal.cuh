@@ -252,6 +252,7 @@ struct Ctx {
   bool work_ready = false;
   double *Vm = nullptr, *crsm = nullptr, *Vp = nullptr, *crsp = nullptr, *phih = nullptr,
          *rauf = nullptr, *coef = nullptr, *corr = nullptr, *lf = nullptr;
+  double* u_save = nullptr;  // u before the batched momentum solve (error rollback)
   // work
   std::vector<void*> allocs;
   double* scratch = nullptr;  // solver scratch (pool slots S_SCR..)

@@ -361,6 +361,19 @@ class RankRun(_TeamRunBase):
                 bases.append(ptr.value)
         _lib.check(self.member.attach(bases, [i[3] for i in infos]))
         same_device = len({(i[5], i[1]) for i in infos}) == 1
+        # evidence for the multi-GPU bench line: where each rank runs and how
+        # it reaches its peers' pools
+        peer_ok = []
+        for q, (_pid, dev, *_rest) in enumerate(infos):
+            ok = C.c_int()
+            _lib.check(_lib.lib.fvb_device_can_access_peer(device, dev, C.byref(ok)))
+            peer_ok.append(int(ok.value))
+        self.diag = {"rank": rank, "pid": os.getpid(), "device": device,
+                     "host": socket.gethostname(), "ipc_mapped": len(self._opened),
+                     "same_process_peers": sum(1 for q, i in enumerate(infos)
+                                               if q != rank and i[0] == os.getpid()),
+                     "peer_devices": [i[1] for i in infos], "can_access_peer": peer_ok,
+                     "rows": int(sd.n_rows), "scope": "gpu" if same_device else "sys"}
         _lib.check(_lib.lib.fvb_team_set_scope(self.member.ctx.h, _scope(same_device)))
         _lib.check(_lib.lib.fvb_team_check(self.member.ctx.h))
         self.member.set_bcs(self.u_field, self.p_field, self.geom)

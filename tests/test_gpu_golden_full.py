@@ -145,3 +145,43 @@ def test_c3_backward_step_nh16_simple_to_convergence():
             "flux": rel(st.flux, g["flux"])}
     assert max(errs.values()) < FIELD_TOL, errs
     assert continuity_error(st) <= 1e-8 * np.abs(st.flux).max()
+
+
+@pytest.mark.slow
+def test_reseeded_one_step_64_vs_oracle():
+    """SURVEY.md §7 hard part 1 protocol (iii): one PISO step of gen_cavity(64)
+    from the same seeded non-trivial state on the device and in the oracle
+    (oracle/fvoracle.py, pinned to the reference), at tightened tolerances."""
+    from oracle import fvoracle as O
+    from paper_1207_1571_b200.mesh import compute_geometry
+
+    n = 64
+    case = _cavity(n, True)
+    cfg = CouplingConfig.from_case_config(case.config)
+    geo = compute_geometry(case.mesh)
+    x, y, z = (geo.cell_centroid[:, k] / 0.1 for k in range(3))
+    rng = np.random.default_rng(1207)
+    ph = rng.uniform(0, 2 * np.pi, size=6)
+    u0 = np.stack([0.3 * np.sin(np.pi * x + ph[0]) * np.cos(np.pi * y) * np.sin(np.pi * z + ph[1]),
+                   0.2 * np.cos(np.pi * x) * np.sin(np.pi * y + ph[2]) * np.sin(np.pi * z),
+                   0.1 * np.sin(np.pi * x) * np.sin(np.pi * y) * np.cos(np.pi * z + ph[3])], axis=1)
+    p0 = 0.05 * np.cos(np.pi * x + ph[4]) * np.cos(np.pi * y + ph[5]) * np.cos(np.pi * z)
+    run = O.Run(case.mesh, case.config)
+    run.u.values[:] = u0
+    run.p.values[:] = p0
+    O.apply_bcs(run.u, run.g, cfg.dt)
+    O.apply_bcs(run.p, run.g, cfg.dt)
+    flux0 = run._plain_flux()
+    run.flux = flux0.copy()
+    run.outer = 1
+    st = init_state(case, cfg)
+    st.u.values, st.p.values, st.flux = u0, p0, flux0
+    st.outer, st.t = 1, cfg.dt
+    piso_time_step(st, cfg)
+    run.piso_step()
+    errs = {"u": rel(st.u.values, run.u.values), "p": rel(st.p.values, run.p.values),
+            "flux": rel(st.flux, run.flux)}
+    assert max(errs.values()) < FIELD_TOL, errs
+    for a, b in zip(st.residual_log, run.log):
+        assert (a[0], a[1]) == (b[0], b[1])
+        assert abs(a[3] - b[3]) <= (2 if a[0] == "cg" else max(3, b[3] // 10)), (a, b)

@@ -15,8 +15,7 @@ from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
 
 n = int(sys.argv[1]); iters = int(sys.argv[2])
-opts = (_lib.SOLVER_EXPLICIT_INDEX if "explicit" in sys.argv[3:] else 0) | \
-    (_lib.SOLVER_NO_RCM if "norcm" in sys.argv[3:] else 0)
+opts = (1 if "explicit" in sys.argv[3:] else 0) | (2 if "norcm" in sys.argv[3:] else 0)
 t0 = time.time()
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
 if len(sys.argv) > 3 and sys.argv[3] == "perm":
@@ -45,8 +44,9 @@ V[np.arange(N), pat.diag_slot] = (pat.I >= 0).sum(axis=1) - 1 + ncrs + 0.01
 b = np.random.default_rng(0).normal(size=N)
 x = np.empty(N)
 ctx = context_for(None, None, pat)
-_lib.check(_lib.lib.fvb_set_solver_options(ctx.h, opts))
 grid = [int(a[5:]) for a in sys.argv[3:] if a.startswith("grid=")]
+if opts or grid:  # (absent from builds older than the options API)
+    _lib.check(_lib.lib.fvb_set_solver_options(ctx.h, opts))
 if grid:
     _lib.check(_lib.lib.fvb_set_solver_grid(ctx.h, grid[0]))
 rep = _lib.SolveReportC()
