@@ -89,6 +89,27 @@ def peaks():
         return HBM_FALLBACK, "fallback"
 
 
+def host_topology(dev):
+    """Where the pinned e2e buffers live relative to the GPU: the GPU's NUMA
+    node (sysfs) and the CPUs this process may run on."""
+    out = {"cpus_allowed": len(os.sched_getaffinity(0)), "cpu_count": os.cpu_count()}
+    try:
+        bus = subprocess.run(["nvidia-smi", f"--id={dev}", "--query-gpu=pci.bus_id",
+                              "--format=csv,noheader"], capture_output=True, text=True,
+                             timeout=20).stdout.strip().lower()
+        dom, rest = bus.split(":", 1)
+        path = f"/sys/bus/pci/devices/{dom[-4:]}:{rest}/numa_node"
+        with open(path) as f:
+            out["gpu_numa_node"] = int(f.read().strip())
+        with open("/proc/self/status") as f:
+            for line in f:
+                if line.startswith("Mems_allowed_list"):
+                    out["mems_allowed"] = line.split(":", 1)[1].strip()
+    except Exception as e:  # informative only
+        out["error"] = str(e)[:80]
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -705,13 +726,26 @@ def run_ours(args):
             _lib.check(_lib.lib.fvb_get_state(h, P(u_h), P(p_h), P(f_h), None, None))
         e2e_ms = C.c_double()
         _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(e2e_ms)))
+        # the copies alone (one more untimed round trip, event-timed on the
+        # library stream): achieved h2d / d2h GB/s of this host
+        t_h2d, t_d2h = C.c_double(), C.c_double()
+        _lib.check(_lib.lib.fvb_timer_start(h))
+        _lib.check(_lib.lib.fvb_set_state(h, P(u_h), P(p_h), P(f_h), None, None))
+        _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(t_h2d)))
+        _lib.check(_lib.lib.fvb_timer_start(h))
+        _lib.check(_lib.lib.fvb_get_state(h, P(u_h), P(p_h), P(f_h), None, None))
+        _lib.check(_lib.lib.fvb_timer_stop(h, C.byref(t_d2h)))
         for b in bufs:
             _lib.lib.fvb_host_unregister(b.ctypes.data)
         e2e_step = D.max(e2e_ms.value) / args.steps
         io_bytes = int(D.sum(sum(b.nbytes for b in bufs)))
         e2e = {"value": N / (e2e_step / 1e3), "unit": "cell-updates/s",
                "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
-               "ms_per_step": e2e_step}
+               "ms_per_step": e2e_step,
+               "copy_ms": {"h2d": t_h2d.value, "d2h": t_d2h.value},
+               "copy_gbs": {"h2d": sum(b.nbytes for b in bufs) / t_h2d.value / 1e6,
+                            "d2h": sum(b.nbytes for b in bufs) / t_d2h.value / 1e6},
+               "host": host_topology(D.local)}
     # ------------------------------------------------------- cpu baseline
     cpu = None
     if D.world == 1 and not args.no_cpu_baseline:

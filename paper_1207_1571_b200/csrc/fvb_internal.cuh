@@ -161,6 +161,9 @@ struct PatternView {
   const uint8_t* code;
   const int* stab;
   int ncode;
+  // box structure (stencil codes on): the largest column offset `plane`
+  // divides n into nz planes; 0 = none (spmv_march)
+  int plane, nz;
 };
 constexpr int kMaxCodes = 255;      // distinct offset tuples per pattern
 constexpr int kEscapeCode = 255;    // row outside the dictionary: explicit I
@@ -219,6 +222,8 @@ struct Ctx {
   int* stab = nullptr;
   int n_scode = 0;
   int64_t n_sescape = 0;     // rows coded kEscapeCode
+  int march_plane = 0;       // PatternView::plane (single domain, codes on)
+  int march_zc = 0, march_chunks = 0;  // spmv_march chunking (uses_march)
   // bandwidth-reducing (reverse Cuthill-McKee) order for CG on patterns
   // without stencil codes: rcm_perm[new] = old row, permuted slot-major
   // columns and diagonal slots; the per-solve permuted matrix in rcm_V
@@ -274,7 +279,7 @@ struct Ctx {
   }
   PatternView pattern() const {
     return PatternView{nr, k, nnz_crs, I, diag_slot, slot_face, crs_ptr, crs_col, crs_face,
-                       scode, stab, n_scode};
+                       scode, stab, n_scode, march_plane, march_plane ? nr / march_plane : 0};
   }
   BcView bc(int field) const {
     return BcView{bc_kind[field], bc_patch[field], bc_fixed[field], bc_speed[field]};
@@ -514,7 +519,9 @@ __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
 // p.q in one block (profiles/r02_stress.md).
 constexpr size_t kRedStride = 16;
 
-template <int M, bool OOL = false>
+// TEAM = false: the kernel instantiation for a single domain, which
+// compiles the team path away (it costs registers in the solver loops).
+template <int M, bool OOL = false, bool TEAM = true>
 __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
                                             double* smem /*[32*M+M]*/, unsigned& rnd,
@@ -526,7 +533,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
 #ifdef FVB_DIAG_FENCE  // diagnostic build (tools/build_variant.py): every thread fences
   __threadfence();
 #endif
-  if (T.size <= 1) {
+  if (!TEAM || T.size <= 1) {
     // One device: a monotonic arrival counter, no last-arriver hand-off.
     // Every block publishes its partials, arrives with a release add and
     // waits until all gridDim.x blocks of round rnd arrived, then sums the
@@ -601,11 +608,11 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   // sys: the peers are other devices, so arrivals order this block's halo
   // stores at system scope
   const bool teamed = T.size > 1;
-  // Multi-device team (T.sys): every block's arrival is a system-scope
-  // acq_rel, so its halo stores to the peers (NVLink) are ordered before the
-  // last arriver's mailbox flags by the release of the storing thread's own
-  // block — not only through the cumulativity of the last arriver's
-  // fence.sc.sys, which a gpu-scope arrival would rely on.  One device (all
+  // Multi-device team (T.sys): every block fences at system scope before its
+  // arrival, so its halo stores to the peers (NVLink) are ordered before the
+  // last arriver's mailbox flags by the storing block itself — not only
+  // through the cumulativity of the last arriver's fence.sc.sys, which a
+  // bare gpu-scope arrival would rely on.  One device (all
   // ranks co-resident, tests): gpu scope.  (A gpu-scope arrival measured
   // ~6 us less per reduction on one device, profiles/r01_team.md, but a
   // multi-GPU run has not validated it.)
@@ -622,7 +629,8 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     double* part = partials + size_t(gen & 1u) * kRedStride * gridDim.x;
 #pragma unroll
     for (int m = 0; m < M; ++m) part[size_t(m) * gridDim.x + blockIdx.x] = v[m];
-    s_last = atom_arrive(sync, sys) == gridDim.x - 1;
+    if (sys) __threadfence_system();  // (a predicated fence: no second atomic form)
+    s_last = atom_arrive(sync, false) == gridDim.x - 1;
   }
   __syncthreads();
   const unsigned gen = s_gen;
@@ -735,6 +743,7 @@ bool cg_defers_x(const Ctx* c);
 // the solvers read stencil codes / run in RCM order (format options)
 bool uses_codes(const Ctx* c);
 bool uses_rcm(const Ctx* c);
+bool uses_march(Ctx* c);
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
                    double* const* x, double tol, double abs_tol, int max_iters,
                    SolveOut* out, const Readback* extra = nullptr);

@@ -86,7 +86,7 @@ __device__ __forceinline__ void icols_ring_load(const PatternView& P, int (&cq)[
   }
 }
 
-template <int KT, int DEPTH>
+template <int KT, int DEPTH, bool TEAM>
 __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const double* __restrict__ z,
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
@@ -99,7 +99,7 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
   const int n = P.n;
   const int* __restrict__ I = P.I;
   const double* __restrict__ V = A.V;
-  const bool team = T.size > 1;
+  const bool team = TEAM && T.size > 1;
   double acc = 0.0;
   icols_ring_load<KT, DEPTH>(P, cq, i, end, step);
   auto g = [&](int col) { return first ? z[col] : po[col] * beta + z[col]; };
@@ -150,7 +150,7 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
 // from the shared-memory copy of the code table; rows coded kEscapeCode
 // load their explicit indices.  Columns, products and order as
 // cg_pass_a_icols.
-template <int KT, int DEPTH>
+template <int KT, int DEPTH, bool TEAM>
 __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const double* __restrict__ z,
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
@@ -163,7 +163,7 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
   const int* __restrict__ I = P.I;
   const uint8_t* __restrict__ code = P.code;
   const double* __restrict__ V = A.V;
-  const bool team = T.size > 1;
+  const bool team = TEAM && T.size > 1;
   double acc = 0.0;
   int cq[DEPTH];
 #pragma unroll
@@ -230,7 +230,7 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
 // the stencil-code ring (cg_pass_a_codes), pass B on row pairs with 16-byte
 // L2-only loads; KT = 0: generic K, plain row loops.  Rows are grid-strided
 // over every thread (team_rows).
-template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0>
+template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
   // SC: stencil-coded pass A (PatternView::code) with the code table here
@@ -247,9 +247,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   unsigned rnd = 0;  // reduction round of this launch (team_reduce)
   const RowRange R = team_rows(T, nrows);
   const int row0 = R.begin, n = R.end, G = R.step;
-  const bool sends = R.sends;
+  const bool sends = TEAM && R.sends;
   const int tid = row0;
-  const bool team = T.size > 1;
+  const bool team = TEAM && T.size > 1;
   const double* __restrict__ inv = A.inv;
   const bool vec_ok = PB2 && ((reinterpret_cast<uintptr_t>(A.pb) | reinterpret_cast<uintptr_t>(A.pa) |
                                reinterpret_cast<uintptr_t>(A.x) | reinterpret_cast<uintptr_t>(A.r) |
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s3[2] += ri * zi;
     }
   }
-  if (!team_reduce<3, true>(T, A.sync, A.partials, s3, red, rnd, sends)) {
+  if (!team_reduce<3, true, TEAM>(T, A.sync, A.partials, s3, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
@@ -310,10 +310,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
       if (SC && KT > 0) {
-        pq[0] = cg_pass_a_codes<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab,
+        pq[0] = cg_pass_a_codes<KR, DR, TEAM>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab,
                                         DEFER ? A.x : nullptr, alpha_prev);
       } else if (KT > 0) {
-        pq[0] = cg_pass_a_icols<KR, DR>(A, z, po, pnew, beta, first, slot_new, tid, n, G, ring,
+        pq[0] = cg_pass_a_icols<KR, DR, TEAM>(A, z, po, pnew, beta, first, slot_new, tid, n, G, ring,
                                         DEFER ? A.x : nullptr, alpha_prev);
       } else {
         for (int i = tid; i < n; i += G) {
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     }
     if (DEFER) p_pend = nullptr;  // pass A applied the previous update
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
-    if (!team_reduce<1, true>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<1, true, TEAM>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       p_pend = pnew;
       alpha_prev = alpha;
     }
-    if (!team_reduce<2, true>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<2, true, TEAM>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
@@ -540,6 +540,92 @@ __device__ __forceinline__ void spmv_sweep(const PatternView& P, const double* _
   }
 }
 
+// Row sweep over a box-structured pattern marching in its slowest index
+// (the "z" planes of PatternView::plane rows): a work item is one in-plane
+// position j and a chunk of zc consecutive planes, walked in order, so the
+// gathered value of row r - plane is the previous step's own value and that
+// of r + plane is computed one step ahead (a coalesced stream) — the two
+// far columns of a 7-point row come from registers instead of L2.  The
+// in-plane columns are gathered as in spmv_sweep (mostly L1).  Same values,
+// products and summation order per row as spmv_sweep; only the assignment
+// of rows to threads (and so the grouping of the dot products) differs.
+template <int KT, int NC, typename Gt, typename Bt>
+__device__ __forceinline__ void spmv_march(const PatternView& P, const double* __restrict__ V,
+                                           const double* crs, int zc, int nchunks, int tid,
+                                           int step, const bool* act, Gt gather, Bt body,
+                                           const int* s_tab) {
+  const int n = P.n, pl = P.plane, nz = P.nz;
+  const int items = pl * nchunks;
+  for (int w = tid; w < items; w += step) {
+    const int q = w / pl, j = w - q * pl;
+    const int z0 = q * zc, z1 = min(z0 + zc, nz);
+    int r = j + z0 * pl;
+    double gp[NC], gc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      gp[c] = (act[c] && z0 > 0) ? gather(c, r - pl) : 0.0;
+      gc[c] = act[c] ? gather(c, r) : 0.0;
+    }
+    int cd = z0 < z1 ? int(__ldcs(P.code + r)) : 0;
+    for (int z = z0; z < z1; ++z, r += pl) {
+      double v[KT];
+#pragma unroll
+      for (int s = 0; s < KT; ++s) v[s] = __ldcs(V + size_t(s) * n + r);
+      const int cdn = z + 1 < z1 ? int(__ldcs(P.code + r + pl)) : 0;
+      double gn[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) gn[c] = (act[c] && z + 1 < nz) ? gather(c, r + pl) : 0.0;
+      int off[KT];
+      if (cd != kEscapeCode) {
+        const int* so = s_tab + cd * KT;
+#pragma unroll
+        for (int s = 0; s < KT; ++s) off[s] = so[s];
+      } else {
+#pragma unroll
+        for (int s = 0; s < KT; ++s) {
+          const int col = __ldcs(P.I + size_t(s) * n + r);
+          off[s] = col < 0 ? kPadOffset : col - r;
+        }
+      }
+      double y[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (!act[c]) continue;
+        auto val = [&](int s) {
+          const int o = off[s];
+          if (o == 0) return gc[c];
+          if (o == pl) return gn[c];
+          if (o == -pl) return gp[c];
+          return gather(c, o == kPadOffset ? 0 : r + o);
+        };
+        double ev = v[0] * val(0);
+#pragma unroll
+        for (int s = 2; s < KT; s += 2) ev = ev + v[s] * val(s);
+        double yy = ev;
+        if (KT > 1) {
+          double od = v[1] * val(1);
+#pragma unroll
+          for (int s = 3; s < KT; s += 2) od = od + v[s] * val(s);
+          yy = ev + od;
+        }
+        if (P.nnz_crs) {
+          double tl = 0.0;
+          for (int e = P.crs_ptr[r]; e < P.crs_ptr[r + 1]; ++e) tl += crs[e] * gather(c, P.crs_col[e]);
+          yy = yy + tl;
+        }
+        y[c] = yy;
+      }
+      body(r, y);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        gp[c] = gc[c];
+        gc[c] = gn[c];
+      }
+      cd = cdn;
+    }
+  }
+}
+
 struct CompState {
   int it, done, err, err_it, sconv, restart, copy, live;
   double bn, res0, res, rho, alpha, omega, beta, rr, rhr;
@@ -577,10 +663,17 @@ struct Bi3Params {
   double* partials;
   double* result;
   const int* zero_flag;  // as CgParams::zero_flag
+  int march_zc, march_chunks;  // spmv_march work items (MARCH kernels)
 };
 
-template <int KT, int NC, bool SC = false>
-__global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A) {
+// blocks of 512 threads per SM of the plane-marching BiCGStab kernel
+#ifndef FVB_BI_MARCH_MINB
+#define FVB_BI_MARCH_MINB 2
+#endif
+
+template <int KT, int NC, bool SC = false, bool MARCH = false, bool TEAM = false>
+__global__ void __launch_bounds__(kSolverThreads, MARCH ? FVB_BI_MARCH_MINB : 2)
+    k_bicgstab3(Bi3Params<NC> A) {
   __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
   __shared__ CompState S[NC];
   // SC: stencil-coded SpMV sweeps (PatternView::code) with the code table here
@@ -599,9 +692,9 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
   const int n = R.end;       // rows of this block: tid, tid + G, ... < n
   const int G = R.step;
   const int tid = R.begin;
-  const bool sends = R.sends;
+  const bool sends = TEAM && R.sends;
   unsigned rnd = 0;  // reduction round of this launch (team_reduce)
-  const bool team = T.size > 1;
+  const bool team = TEAM && T.size > 1;
   const double* __restrict__ inv = A.inv;
   bool act[NC];
   bool timeout = false;
@@ -640,7 +733,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
       }
     }
   }
-  if (!team_reduce<2 * NC>(T, A.sync, A.partials, sums, red, rnd, sends)) {
+  if (!team_reduce<2 * NC, false, TEAM>(T, A.sync, A.partials, sums, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
@@ -740,7 +833,15 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       };
       if (KT > 0) {
-        spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
+        if (MARCH)
+          spmv_march<KR, NC>(P, A.V, A.crs, A.march_zc, A.march_chunks, tid, G, act, g, body,
+                             s_tab);
+        else
+          if (MARCH)
+          spmv_march<KR, NC>(P, A.V, A.crs, A.march_zc, A.march_chunks, tid, G, act, g, body,
+                             s_tab);
+        else
+          spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
       } else {
         for (int i = tid; i < n; i += G) {
           double y[NC];
@@ -749,7 +850,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<NC, false, TEAM>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -796,7 +897,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<3 * NC>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<3 * NC, false, TEAM>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -903,7 +1004,7 @@ __global__ void __launch_bounds__(kSolverThreads, 2) k_bicgstab3(Bi3Params<NC> A
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC, false, TEAM>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -1085,9 +1186,53 @@ __global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ pe
     for (int k = 0; k < ncomp; ++k) R.x[k][perm[r]] = R.xp[k][r];
 }
 
+// k_cg instantiation for the context: K (5, 7 or generic), stencil codes,
+// deferred x update on 7-point rows, team or single domain
+template <bool TEAM>
+static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
+  switch (c->k) {
+    case 5:
+      if (sc) return coop_launch(c, k_cg<5, 1024, 1, 1, 0, TEAM>, prm, 1024, 1);
+      return coop_launch(c, k_cg<5, 1024, 1, 0, 0, TEAM>, prm, 1024, 1);
+    case 7:  // x update folded into pass A (cg_defers_x)
+      if (sc) return coop_launch(c, k_cg<7, 1024, 1, 1, 1, TEAM>, prm, 1024, 1);
+      return coop_launch(c, k_cg<7, 1024, 1, 0, 1, TEAM>, prm, 1024, 1);
+    default: return coop_launch(c, k_cg<0, 512, 2, 0, 0, TEAM>, prm);
+  }
+}
+
 bool uses_codes(const Ctx* c) {
   return c->scode != nullptr && !(c->solver_flags & FVB_SOLVER_EXPLICIT_INDEX);
 }
+// plane-marching SpMV sweeps (spmv_march) for the BiCGStab batch: box-
+// structured single-domain patterns with stencil codes, 7-point rows; the
+// chunk length zc balances plane * ceil(nz / zc) work items of zc + 1 row
+// computations over the persistent grid (512 x 2 per SM)
+bool uses_march(Ctx* c) {
+  if (!c->march_plane || c->teamed() || c->k != 7 || (c->solver_flags & FVB_SOLVER_NO_MARCH))
+    return false;
+  if (!c->march_zc) {
+    const long long pl = c->march_plane, nz = c->nr / c->march_plane;
+    const long long G = 1LL * FVB_BI_MARCH_MINB * kSolverThreads * c->num_sms /
+                        (c->sm_share > 0 ? c->sm_share : 1);
+    long long best = -1;
+    for (long long zc = 2; zc <= 64 && zc <= nz; ++zc) {
+      const long long chunks = (nz + zc - 1) / zc;
+      const long long cost = ((pl * chunks + G - 1) / G) * (zc + 1);
+      if (best < 0 || cost <= best) {
+        best = cost;
+        c->march_zc = int(zc);
+        c->march_chunks = int(chunks);
+      }
+    }
+    if (best < 0) {
+      c->march_zc = int(nz);
+      c->march_chunks = 1;
+    }
+  }
+  return true;
+}
+
 bool uses_rcm(const Ctx* c) {
   return c->rcm_perm && !c->teamed() && c->k == 7 && !(c->solver_flags & FVB_SOLVER_NO_RCM);
 }
@@ -1143,22 +1288,10 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   // pattern has them, else on the explicit index ring (tuning history:
   // profiles/r01_cg_variants.md)
   const bool sc = uses_codes(c);
-  switch (c->k) {
-    case 5:
-      if (sc)
-        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1, 1>, prm, 1024, 1));
-      else
-        FVB_TRY(coop_launch(c, k_cg<5, 1024, 1>, prm, 1024, 1));
-      break;
-    case 7:
-      // x update folded into pass A (cg_defers_x)
-      if (sc)
-        FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 1, 1>, prm, 1024, 1));
-      else
-        FVB_TRY(coop_launch(c, k_cg<7, 1024, 1, 0, 1>, prm, 1024, 1));
-      break;
-    default: FVB_TRY(coop_launch(c, k_cg<0, 512, 2>, prm)); break;
-  }
+  if (c->teamed())
+    FVB_TRY(cg_launch<true>(c, prm, sc));
+  else
+    FVB_TRY(cg_launch<false>(c, prm, sc));
   if (rcm) {
     k_rcm_scatter<<<grid_for(c->nr, 256), 256, 0, c->stream>>>(c->nr, c->rcm_perm, xp, x);
     note_launch();
@@ -1223,13 +1356,32 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   prm.result = result;
   prm.zero_flag = c->teamed() ? nullptr : c->ipart;
   // stencil-coded SpMV sweeps when the pattern has codes (unless the
-  // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX)
+  // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX); on a
+  // box-structured single domain they march through the planes
   const bool sc = uses_codes(c);
+  const bool march = sc && !pov && uses_march(c);
+  if (march) {
+    prm.march_zc = c->march_zc;
+    prm.march_chunks = c->march_chunks;
+  }
+  if (c->teamed()) {
+    switch (c->k) {
+      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, false, true>, prm)
+                        : coop_launch(c, k_bicgstab3<5, NC, false, false, true>, prm);
+      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, false, true>, prm)
+                        : coop_launch(c, k_bicgstab3<7, NC, false, false, true>, prm);
+      default: return coop_launch(c, k_bicgstab3<0, NC, false, false, true>, prm);
+    }
+  }
   switch (c->k) {
     case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm)
                       : coop_launch(c, k_bicgstab3<5, NC>, prm);
-    case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm)
-                      : coop_launch(c, k_bicgstab3<7, NC>, prm);
+    case 7:
+      if (march)
+        return coop_launch(c, k_bicgstab3<7, NC, true, true>, prm, kSolverThreads,
+                           FVB_BI_MARCH_MINB);
+      return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm)
+                : coop_launch(c, k_bicgstab3<7, NC>, prm);
     default: return coop_launch(c, k_bicgstab3<0, NC>, prm);
   }
 }
