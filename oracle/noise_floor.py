@@ -7,7 +7,7 @@ the golden run (tests/golden/full_*.npz) when judging the device counts.
     python oracle/noise_floor.py c2|c4 MODE [steps]
 
 MODE "seqspmv": smvp summed slot by slot (y = V0 x0; y += Vk xk) instead of
-numpy's einsum grouping; MODE "blas8": OpenBLAS with 8 threads (ddot split
+numpy's einsum grouping; MODE "blasT": OpenBLAS with T threads (ddot split
 differently) instead of 1.  Output: tests/golden/floor_<case>_<mode>.json.
 """
 import json
@@ -15,7 +15,7 @@ import os
 import sys
 
 MODE = sys.argv[2]
-os.environ["OPENBLAS_NUM_THREADS"] = "8" if MODE == "blas8" else "1"
+os.environ["OPENBLAS_NUM_THREADS"] = MODE[4:] if MODE.startswith("blas") else "1"
 
 import numpy as np  # noqa: E402
 

@@ -868,13 +868,6 @@ static int build_stencil_codes(Ctx* c, const std::vector<int>& Is, size_t nn, si
   FVB_CUDA(cudaMemcpy(c->stab, tab.data(), tab.size() * sizeof(int), cudaMemcpyHostToDevice));
   c->n_scode = int(tab.size() / kk);
   c->n_sescape = int64_t(escapes);
-  // box structure for the plane-marching SpMV sweeps: the largest column
-  // offset is the plane stride when it divides the rows into >= 2 planes
-  int plane = 0;
-  for (int o : tab)
-    if (o != kPadOffset && o > plane) plane = o;
-  if (c->nc == c->nr && plane > 1 && nn % size_t(plane) == 0 && nn / size_t(plane) >= 2)
-    c->march_plane = plane;
   return FVB_OK;
 }
 }  // namespace fvb
@@ -1596,7 +1589,7 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
 }
 
 int fvb_set_solver_options(fvb_ctx* h, int flags) {
-  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM | FVB_SOLVER_NO_MARCH)) {
+  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM)) {
     fvb_set_error("unknown solver option bits 0x%x", flags);
     return FVB_E_ARG;
   }

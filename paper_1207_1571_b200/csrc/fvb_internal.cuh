@@ -161,9 +161,6 @@ struct PatternView {
   const uint8_t* code;
   const int* stab;
   int ncode;
-  // box structure (stencil codes on): the largest column offset `plane`
-  // divides n into nz planes; 0 = none (spmv_march)
-  int plane, nz;
 };
 constexpr int kMaxCodes = 255;      // distinct offset tuples per pattern
 constexpr int kEscapeCode = 255;    // row outside the dictionary: explicit I
@@ -222,8 +219,6 @@ struct Ctx {
   int* stab = nullptr;
   int n_scode = 0;
   int64_t n_sescape = 0;     // rows coded kEscapeCode
-  int march_plane = 0;       // PatternView::plane (single domain, codes on)
-  int march_zc = 0, march_chunks = 0;  // spmv_march chunking (uses_march)
   // bandwidth-reducing (reverse Cuthill-McKee) order for CG on patterns
   // without stencil codes: rcm_perm[new] = old row, permuted slot-major
   // columns and diagonal slots; the per-solve permuted matrix in rcm_V
@@ -279,7 +274,7 @@ struct Ctx {
   }
   PatternView pattern() const {
     return PatternView{nr, k, nnz_crs, I, diag_slot, slot_face, crs_ptr, crs_col, crs_face,
-                       scode, stab, n_scode, march_plane, march_plane ? nr / march_plane : 0};
+                       scode, stab, n_scode};
   }
   BcView bc(int field) const {
     return BcView{bc_kind[field], bc_patch[field], bc_fixed[field], bc_speed[field]};
@@ -743,7 +738,6 @@ bool cg_defers_x(const Ctx* c);
 // the solvers read stencil codes / run in RCM order (format options)
 bool uses_codes(const Ctx* c);
 bool uses_rcm(const Ctx* c);
-bool uses_march(Ctx* c);
 int bicgstab_solve(Ctx* c, MatView A, int ncomp, const double* const* b,
                    double* const* x, double tol, double abs_tol, int max_iters,
                    SolveOut* out, const Readback* extra = nullptr);

@@ -200,9 +200,18 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
         ci[s] = c < 0 ? 0 : c;
       }
     }
+    // issue every gather of the row before the first use (memory-level
+    // parallelism: the compiler otherwise interleaves load-use pairs)
+    double zg[KT], pg[KT];
+#pragma unroll
+    for (int s = 0; s < KT; ++s) zg[s] = z[ci[s]];
+    if (!first) {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) pg[s] = po[ci[s]];
+    }
     double pr[KT];
 #pragma unroll
-    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * g(ci[s]);
+    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * (first ? zg[s] : pg[s] * beta + zg[s]);
     double ev = pr[0];
 #pragma unroll
     for (int s = 2; s < KT; s += 2) ev = ev + pr[s];
@@ -540,92 +549,6 @@ __device__ __forceinline__ void spmv_sweep(const PatternView& P, const double* _
   }
 }
 
-// Row sweep over a box-structured pattern marching in its slowest index
-// (the "z" planes of PatternView::plane rows): a work item is one in-plane
-// position j and a chunk of zc consecutive planes, walked in order, so the
-// gathered value of row r - plane is the previous step's own value and that
-// of r + plane is computed one step ahead (a coalesced stream) — the two
-// far columns of a 7-point row come from registers instead of L2.  The
-// in-plane columns are gathered as in spmv_sweep (mostly L1).  Same values,
-// products and summation order per row as spmv_sweep; only the assignment
-// of rows to threads (and so the grouping of the dot products) differs.
-template <int KT, int NC, typename Gt, typename Bt>
-__device__ __forceinline__ void spmv_march(const PatternView& P, const double* __restrict__ V,
-                                           const double* crs, int zc, int nchunks, int tid,
-                                           int step, const bool* act, Gt gather, Bt body,
-                                           const int* s_tab) {
-  const int n = P.n, pl = P.plane, nz = P.nz;
-  const int items = pl * nchunks;
-  for (int w = tid; w < items; w += step) {
-    const int q = w / pl, j = w - q * pl;
-    const int z0 = q * zc, z1 = min(z0 + zc, nz);
-    int r = j + z0 * pl;
-    double gp[NC], gc[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      gp[c] = (act[c] && z0 > 0) ? gather(c, r - pl) : 0.0;
-      gc[c] = act[c] ? gather(c, r) : 0.0;
-    }
-    int cd = z0 < z1 ? int(__ldcs(P.code + r)) : 0;
-    for (int z = z0; z < z1; ++z, r += pl) {
-      double v[KT];
-#pragma unroll
-      for (int s = 0; s < KT; ++s) v[s] = __ldcs(V + size_t(s) * n + r);
-      const int cdn = z + 1 < z1 ? int(__ldcs(P.code + r + pl)) : 0;
-      double gn[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) gn[c] = (act[c] && z + 1 < nz) ? gather(c, r + pl) : 0.0;
-      int off[KT];
-      if (cd != kEscapeCode) {
-        const int* so = s_tab + cd * KT;
-#pragma unroll
-        for (int s = 0; s < KT; ++s) off[s] = so[s];
-      } else {
-#pragma unroll
-        for (int s = 0; s < KT; ++s) {
-          const int col = __ldcs(P.I + size_t(s) * n + r);
-          off[s] = col < 0 ? kPadOffset : col - r;
-        }
-      }
-      double y[NC];
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (!act[c]) continue;
-        auto val = [&](int s) {
-          const int o = off[s];
-          if (o == 0) return gc[c];
-          if (o == pl) return gn[c];
-          if (o == -pl) return gp[c];
-          return gather(c, o == kPadOffset ? 0 : r + o);
-        };
-        double ev = v[0] * val(0);
-#pragma unroll
-        for (int s = 2; s < KT; s += 2) ev = ev + v[s] * val(s);
-        double yy = ev;
-        if (KT > 1) {
-          double od = v[1] * val(1);
-#pragma unroll
-          for (int s = 3; s < KT; s += 2) od = od + v[s] * val(s);
-          yy = ev + od;
-        }
-        if (P.nnz_crs) {
-          double tl = 0.0;
-          for (int e = P.crs_ptr[r]; e < P.crs_ptr[r + 1]; ++e) tl += crs[e] * gather(c, P.crs_col[e]);
-          yy = yy + tl;
-        }
-        y[c] = yy;
-      }
-      body(r, y);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        gp[c] = gc[c];
-        gc[c] = gn[c];
-      }
-      cd = cdn;
-    }
-  }
-}
-
 struct CompState {
   int it, done, err, err_it, sconv, restart, copy, live;
   double bn, res0, res, rho, alpha, omega, beta, rr, rhr;
@@ -663,17 +586,15 @@ struct Bi3Params {
   double* partials;
   double* result;
   const int* zero_flag;  // as CgParams::zero_flag
-  int march_zc, march_chunks;  // spmv_march work items (MARCH kernels)
 };
 
-// blocks of 512 threads per SM of the plane-marching BiCGStab kernel
-#ifndef FVB_BI_MARCH_MINB
-#define FVB_BI_MARCH_MINB 2
+// resident 512-thread blocks per SM of the BiCGStab kernel (64 registers)
+#ifndef FVB_BI_MINB
+#define FVB_BI_MINB 2
 #endif
 
-template <int KT, int NC, bool SC = false, bool MARCH = false, bool TEAM = false>
-__global__ void __launch_bounds__(kSolverThreads, MARCH ? FVB_BI_MARCH_MINB : 2)
-    k_bicgstab3(Bi3Params<NC> A) {
+template <int KT, int NC, bool SC = false, bool TEAM = false>
+__global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Params<NC> A) {
   __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
   __shared__ CompState S[NC];
   // SC: stencil-coded SpMV sweeps (PatternView::code) with the code table here
@@ -833,15 +754,7 @@ __global__ void __launch_bounds__(kSolverThreads, MARCH ? FVB_BI_MARCH_MINB : 2)
         }
       };
       if (KT > 0) {
-        if (MARCH)
-          spmv_march<KR, NC>(P, A.V, A.crs, A.march_zc, A.march_chunks, tid, G, act, g, body,
-                             s_tab);
-        else
-          if (MARCH)
-          spmv_march<KR, NC>(P, A.V, A.crs, A.march_zc, A.march_chunks, tid, G, act, g, body,
-                             s_tab);
-        else
-          spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
+        spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
       } else {
         for (int i = tid; i < n; i += G) {
           double y[NC];
@@ -1204,35 +1117,6 @@ static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
 bool uses_codes(const Ctx* c) {
   return c->scode != nullptr && !(c->solver_flags & FVB_SOLVER_EXPLICIT_INDEX);
 }
-// plane-marching SpMV sweeps (spmv_march) for the BiCGStab batch: box-
-// structured single-domain patterns with stencil codes, 7-point rows; the
-// chunk length zc balances plane * ceil(nz / zc) work items of zc + 1 row
-// computations over the persistent grid (512 x 2 per SM)
-bool uses_march(Ctx* c) {
-  if (!c->march_plane || c->teamed() || c->k != 7 || (c->solver_flags & FVB_SOLVER_NO_MARCH))
-    return false;
-  if (!c->march_zc) {
-    const long long pl = c->march_plane, nz = c->nr / c->march_plane;
-    const long long G = 1LL * FVB_BI_MARCH_MINB * kSolverThreads * c->num_sms /
-                        (c->sm_share > 0 ? c->sm_share : 1);
-    long long best = -1;
-    for (long long zc = 2; zc <= 64 && zc <= nz; ++zc) {
-      const long long chunks = (nz + zc - 1) / zc;
-      const long long cost = ((pl * chunks + G - 1) / G) * (zc + 1);
-      if (best < 0 || cost <= best) {
-        best = cost;
-        c->march_zc = int(zc);
-        c->march_chunks = int(chunks);
-      }
-    }
-    if (best < 0) {
-      c->march_zc = int(nz);
-      c->march_chunks = 1;
-    }
-  }
-  return true;
-}
-
 bool uses_rcm(const Ctx* c) {
   return c->rcm_perm && !c->teamed() && c->k == 7 && !(c->solver_flags & FVB_SOLVER_NO_RCM);
 }
@@ -1356,33 +1240,23 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   prm.result = result;
   prm.zero_flag = c->teamed() ? nullptr : c->ipart;
   // stencil-coded SpMV sweeps when the pattern has codes (unless the
-  // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX); on a
-  // box-structured single domain they march through the planes
+  // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX)
   const bool sc = uses_codes(c);
-  const bool march = sc && !pov && uses_march(c);
-  if (march) {
-    prm.march_zc = c->march_zc;
-    prm.march_chunks = c->march_chunks;
-  }
   if (c->teamed()) {
     switch (c->k) {
-      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, false, true>, prm)
-                        : coop_launch(c, k_bicgstab3<5, NC, false, false, true>, prm);
-      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, false, true>, prm)
-                        : coop_launch(c, k_bicgstab3<7, NC, false, false, true>, prm);
-      default: return coop_launch(c, k_bicgstab3<0, NC, false, false, true>, prm);
+      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true>, prm, kSolverThreads, FVB_BI_MINB)
+                        : coop_launch(c, k_bicgstab3<5, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true>, prm, kSolverThreads, FVB_BI_MINB)
+                        : coop_launch(c, k_bicgstab3<7, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+      default: return coop_launch(c, k_bicgstab3<0, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
     }
   }
   switch (c->k) {
-    case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm)
-                      : coop_launch(c, k_bicgstab3<5, NC>, prm);
-    case 7:
-      if (march)
-        return coop_launch(c, k_bicgstab3<7, NC, true, true>, prm, kSolverThreads,
-                           FVB_BI_MARCH_MINB);
-      return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm)
-                : coop_launch(c, k_bicgstab3<7, NC>, prm);
-    default: return coop_launch(c, k_bicgstab3<0, NC>, prm);
+    case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm, kSolverThreads, FVB_BI_MINB)
+                      : coop_launch(c, k_bicgstab3<5, NC>, prm, kSolverThreads, FVB_BI_MINB);
+    case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm, kSolverThreads, FVB_BI_MINB)
+                      : coop_launch(c, k_bicgstab3<7, NC>, prm, kSolverThreads, FVB_BI_MINB);
+    default: return coop_launch(c, k_bicgstab3<0, NC>, prm, kSolverThreads, FVB_BI_MINB);
   }
 }
 

@@ -328,33 +328,3 @@ def test_rcm_ordered_bicgstab_single_and_batched():
         assert np.linalg.norm(B[:, c] - M @ x1) <= 1e-8 * np.linalg.norm(B[:, c])
     _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, None, None, None, C.byref(r1c)))
     assert r1c.value - r0.value == 4  # one batch + three single solves
-
-
-@pytest.mark.parametrize("crs_tail", [False, True])
-def test_bicgstab_plane_march_matches_row_sweep(crs_tail):
-    # box-structured patterns: the batched BiCGStab SpMV sweeps march through
-    # the z planes (far columns from registers); same row products as the
-    # row-by-row sweep (FVB_SOLVER_NO_MARCH), only the dot-product grouping
-    # differs: counts +-1, solutions to rounding.  crs_tail: escaped rows
-    # and a CRS tail inside the march.
-    import ctypes as C
-    from paper_1207_1571_b200 import _lib
-    from paper_1207_1571_b200.device import context_for
-
-    rng = np.random.default_rng(5)
-    p, A, M = _box_operator(24, crs_tail, rng)
-    N = p.n
-    B = rng.normal(size=(N, 3))
-    cfg = SolveConfig(tolerance=1e-10, max_iters=2000)
-    ctx = context_for(None, None, p)
-    X1, r1 = bicgstab_batched(A, B, np.zeros((N, 3)), cfg)
-    _lib.check(_lib.lib.fvb_set_solver_options(ctx.h, _lib.SOLVER_NO_MARCH))
-    try:
-        X2, r2 = bicgstab_batched(A, B, np.zeros((N, 3)), cfg)
-    finally:
-        _lib.check(_lib.lib.fvb_set_solver_options(ctx.h, 0))
-    for c in range(3):
-        assert r1[c].converged and r2[c].converged
-        assert abs(r1[c].iterations - r2[c].iterations) <= 1
-        assert rel(X1[:, c], X2[:, c]) < 1e-8
-        assert np.linalg.norm(B[:, c] - M @ X1[:, c]) <= 1e-9 * np.linalg.norm(B[:, c])

@@ -2,10 +2,9 @@
 Jacobi-BiCGStab on a convection-diffusion-like nonsymmetric matrix (K = 7)
 through fvb_op_bicgstab_batched; prints device time per batched iteration
 and the algorithmic HBM rate (600 B per row per batched iteration).
-Usage: python tools/bi_micro.py N ITERS [crs] [explicit] [nomarch]
+Usage: python tools/bi_micro.py N ITERS [crs] [explicit]
 "crs" adds long-range couplings that spill into the CRS tail; "explicit"
-makes the SpMV sweeps read int32 indices instead of stencil codes, "nomarch"
-sweeps row by row instead of marching through the planes
+makes the SpMV sweeps read int32 indices instead of stencil codes
 (fvb_set_solver_options)."""
 import ctypes as C, hashlib, json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
@@ -16,7 +15,7 @@ from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
 
 n = int(sys.argv[1]); iters = int(sys.argv[2])
-opts = (1 if "explicit" in sys.argv[3:] else 0) | (4 if "nomarch" in sys.argv[3:] else 0)
+opts = 1 if "explicit" in sys.argv[3:] else 0
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
 crs_mode = "crs" in sys.argv[3:]
 if crs_mode:
