@@ -12,8 +12,15 @@ from /root/reference's own run_case / piso_time_step).
   counts over the first sweeps (uz of the one-cell-thick mesh excluded, as
   SURVEY.md §7 prescribes: its rhs is round-off).
 * C4 perturbed + randomly renumbered 126^3 cavity (2,000,376 cells; the
-  device solvers run in RCM order), one PISO step: fields at tight
-  tolerances, counts at defaults.
+  device solvers run in RCM order): one PISO step's fields at tight
+  tolerances, two steps' counts at defaults.
+
+Counts at default tolerances are judged around the spread of the
+reference's OWN counts under 1-ulp reorderings of its arithmetic (OpenBLAS
+thread count, SpMV summation order; tests/golden/floor_*.json from
+oracle/noise_floor.py), as SURVEY.md §7 hard part 1 prescribes: e.g. the
+step-1 ux BiCGStab solve of C2 takes 67, 69 or 70 iterations in the
+reference depending on that order alone.
 """
 
 import os
@@ -41,12 +48,38 @@ def _log_rows(names, log):
             for nm, r in zip(names, log)]
 
 
-def _check_counts(mine, ref, skip_uz=False):
-    """CG +-1, BiCGStab +-2 per solve, same solve sequence."""
+def _check_counts(mine, ref, skip_uz=False, spread=None):
+    """CG +-1, BiCGStab +-2 per solve, same solve sequence.  spread: per
+    solve (lo, hi) of the reference's own counts under 1-ulp reorderings
+    (tests/golden/floor_*.json, oracle/noise_floor.py; SURVEY.md §7 hard part
+    1: counts are judged next to the CPU-vs-CPU floor): the bound then
+    applies around [lo, hi] instead of the single golden count."""
     assert [(a[0], a[1], a[2]) for a in mine] == [(b[0], b[1], b[2]) for b in ref]
-    bad = [(a, b) for a, b in zip(mine, ref)
-           if not (skip_uz and a[1] == "uz") and abs(a[3] - b[3]) > (1 if a[0] == "cg" else 2)]
+    bad = []
+    for j, (a, b) in enumerate(zip(mine, ref)):
+        if skip_uz and a[1] == "uz":
+            continue
+        lo, hi = spread[j] if spread else (b[3], b[3])
+        tol = 1 if a[0] == "cg" else 2
+        if not (lo - tol <= a[3] <= hi + tol):
+            bad.append((a, b, (lo, hi)))
     assert not bad, bad
+
+
+def _floor_spread(case, step, ref):
+    """(lo, hi) per solve of step `step` over the golden run and every
+    committed reference floor run of `case`."""
+    import glob
+    import json
+
+    counts = [[r[3]] for r in ref]
+    for path in sorted(glob.glob(os.path.join(GOLD, f"floor_{case}_*.json"))):
+        with open(path) as f:
+            steps = json.load(f)["steps"]
+        if step < len(steps):
+            for j, row in enumerate(steps[step]):
+                counts[j].append(int(row[2]))
+    return [(min(c), max(c)) for c in counts]
 
 
 def _cavity(n, tight):
@@ -99,8 +132,8 @@ def test_c2_cavity128_fields_tight_tolerances():
 @pytest.mark.slow
 def test_c2_cavity128_iteration_counts_defaults():
     g = _gold("c2_default")
-    for _err, rows, ref, cont, fmax in _steps(_cavity(128, False), g):
-        _check_counts(rows, ref)
+    for s, (_err, rows, ref, cont, fmax) in enumerate(_steps(_cavity(128, False), g)):
+        _check_counts(rows, ref, spread=_floor_spread("c2", s, ref))
         assert cont <= 1e-8 * fmax
 
 
@@ -122,8 +155,8 @@ def test_c4_perturbed_126_fields_tight_tolerances_rcm():
 @pytest.mark.slow
 def test_c4_perturbed_126_iteration_counts_defaults_rcm():
     g = _gold("c4_default")
-    for _err, rows, ref, cont, fmax in _steps(_c4(False), g):
-        _check_counts(rows, ref)
+    for s, (_err, rows, ref, cont, fmax) in enumerate(_steps(_c4(False), g)):
+        _check_counts(rows, ref, spread=_floor_spread("c4", s, ref))
         assert cont <= 1e-8 * fmax
 
 
