@@ -190,7 +190,7 @@ _sig("fvb_sync", I, vp)
 _sig("fvb_set_solver_options", I, vp, C.c_int)
 _sig("fvb_set_solver_grid", I, vp, C.c_int)
 _sig("fvb_device_can_access_peer", I, C.c_int, C.c_int, C.POINTER(C.c_int))
-SOLVER_EXPLICIT_INDEX, SOLVER_NO_RCM = 1, 2
+SOLVER_EXPLICIT_INDEX, SOLVER_NO_RCM, SOLVER_NO_CLUSTER = 1, 2, 4
 _sig("fvb_pattern_codes", I, vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int),
      C.POINTER(C.c_int64))
 _sig("fvb_launch_count", C.c_ulonglong)

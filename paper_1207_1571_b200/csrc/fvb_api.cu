@@ -1589,7 +1589,7 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
 }
 
 int fvb_set_solver_options(fvb_ctx* h, int flags) {
-  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM)) {
+  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM | FVB_SOLVER_NO_CLUSTER)) {
     fvb_set_error("unknown solver option bits 0x%x", flags);
     return FVB_E_ARG;
   }

@@ -239,7 +239,8 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
 // the stencil-code ring (cg_pass_a_codes), pass B on row pairs with 16-byte
 // L2-only loads; KT = 0: generic K, plain row loops.  Rows are grid-strided
 // over every thread (team_rows).
-template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false>
+template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false,
+          bool CLUSTER = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   __shared__ double red[32 * 3 + 3];
   // SC: stencil-coded pass A (PatternView::code) with the code table here
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       s3[2] += ri * zi;
     }
   }
-  if (!team_reduce<3, true, TEAM>(T, A.sync, A.partials, s3, red, rnd, sends)) {
+  if (!team_reduce<3, true, TEAM, CLUSTER>(T, A.sync, A.partials, s3, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     }
     if (DEFER) p_pend = nullptr;  // pass A applied the previous update
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
-    if (!team_reduce<1, true, TEAM>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<1, true, TEAM, CLUSTER>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
       p_pend = pnew;
       alpha_prev = alpha;
     }
-    if (!team_reduce<2, true, TEAM>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<2, true, TEAM, CLUSTER>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
@@ -593,7 +594,7 @@ struct Bi3Params {
 #define FVB_BI_MINB 2
 #endif
 
-template <int KT, int NC, bool SC = false, bool TEAM = false>
+template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false>
 __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Params<NC> A) {
   __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
   __shared__ CompState S[NC];
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
       }
     }
   }
-  if (!team_reduce<2 * NC, false, TEAM>(T, A.sync, A.partials, sums, red, rnd, sends)) {
+  if (!team_reduce<2 * NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, sums, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
@@ -763,7 +764,7 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC, false, TEAM>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -810,7 +811,7 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<3 * NC, false, TEAM>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<3 * NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -917,7 +918,7 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC, false, TEAM>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -989,6 +990,65 @@ int coop_launch(Ctx* c, K kernel, Args& args, int threads = kSolverThreads, int 
                                          params, 0, c->stream));
   }
   return FVB_OK;
+}
+
+// Small single-domain systems: the persistent solver runs as ONE thread-
+// block cluster of `blocks` CTAs (cluster_reduce instead of grid barriers).
+// The cluster size (<= 16, non-portable above 8) is what the device can
+// co-schedule for this kernel; 0 means no cluster launch is possible.
+template <typename K>
+int cluster_blocks(Ctx* c, K kernel, int threads, int want) {
+  int& cmax = c->cluster_max[threads >= 1024 ? 1 : 0];
+  if (cmax < 0) {
+    cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(threads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxPotentialClusterSize(&n, (const void*)kernel, &cfg) != cudaSuccess) n = 0;
+    cudaGetLastError();
+    cmax = n > 16 ? 16 : n;
+  }
+  return want <= cmax ? want : cmax;
+}
+
+template <typename K, typename Args>
+int cluster_launch(Ctx* c, K kernel, Args& args, int threads, int blocks) {
+  FVB_CUDA(cudaFuncSetAttribute((const void*)kernel,
+                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = unsigned(blocks);
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  fvb::note_launch();
+  FVB_CUDA(cudaLaunchKernelEx(&cfg, kernel, args));
+  return FVB_OK;
+}
+
+// cluster size for a single-domain solve of nr rows with `threads`-thread
+// CTAs: about two rows per thread, at least 2 CTAs, none when the system is
+// large (the full grid wins above ~40k rows, tools/cg_micro.py) or fits one
+// block (block barriers), or the context asks for the grid path
+inline int cluster_want(const Ctx* c, int threads) {
+  if (c->teamed() || (c->solver_flags & FVB_SOLVER_NO_CLUSTER) || c->sm_share > 1) return 0;
+  if (c->nr <= 4 * threads || c->nr > kClusterMaxRows) return 0;
+  if (c->solver_max_blocks > 0) return 0;  // an explicit grid cap wins
+  int b = (c->nr + 2 * threads - 1) / (2 * threads);
+  return b < 2 ? 2 : (b > 16 ? 16 : b);
 }
 
 // Inverse diagonal of the owned rows, and the first zero-diagonal row into
@@ -1103,6 +1163,19 @@ __global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ pe
 // deferred x update on 7-point rows, team or single domain
 template <bool TEAM>
 static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
+  if (!TEAM && (c->k == 7 || c->k == 5)) {
+    const int want = cluster_want(c, 1024);
+    const int nb = want ? (c->k == 7 ? cluster_blocks(c, k_cg<7, 1024, 1, 1, 1, false, true>, 1024, want)
+                                     : cluster_blocks(c, k_cg<5, 1024, 1, 1, 0, false, true>, 1024, want))
+                        : 0;
+    if (nb >= 2) {
+      if (c->k == 7)
+        return sc ? cluster_launch(c, k_cg<7, 1024, 1, 1, 1, false, true>, prm, 1024, nb)
+                  : cluster_launch(c, k_cg<7, 1024, 1, 0, 1, false, true>, prm, 1024, nb);
+      return sc ? cluster_launch(c, k_cg<5, 1024, 1, 1, 0, false, true>, prm, 1024, nb)
+                : cluster_launch(c, k_cg<5, 1024, 1, 0, 0, false, true>, prm, 1024, nb);
+    }
+  }
   switch (c->k) {
     case 5:
       if (sc) return coop_launch(c, k_cg<5, 1024, 1, 1, 0, TEAM>, prm, 1024, 1);
@@ -1249,6 +1322,22 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
       case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true>, prm, kSolverThreads, FVB_BI_MINB)
                         : coop_launch(c, k_bicgstab3<7, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
       default: return coop_launch(c, k_bicgstab3<0, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+    }
+  }
+  if (c->k == 7 || c->k == 5) {
+    const int want = cluster_want(c, kSolverThreads);
+    const int nb = want ? (c->k == 7
+                               ? cluster_blocks(c, k_bicgstab3<7, NC, true, false, true>,
+                                                kSolverThreads, want)
+                               : cluster_blocks(c, k_bicgstab3<5, NC, true, false, true>,
+                                                kSolverThreads, want))
+                        : 0;
+    if (nb >= 2) {
+      if (c->k == 7)
+        return sc ? cluster_launch(c, k_bicgstab3<7, NC, true, false, true>, prm, kSolverThreads, nb)
+                  : cluster_launch(c, k_bicgstab3<7, NC, false, false, true>, prm, kSolverThreads, nb);
+      return sc ? cluster_launch(c, k_bicgstab3<5, NC, true, false, true>, prm, kSolverThreads, nb)
+                : cluster_launch(c, k_bicgstab3<5, NC, false, false, true>, prm, kSolverThreads, nb);
     }
   }
   switch (c->k) {

@@ -15,7 +15,7 @@ from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
 
 n = int(sys.argv[1]); iters = int(sys.argv[2])
-opts = 1 if "explicit" in sys.argv[3:] else 0
+opts = (1 if "explicit" in sys.argv[3:] else 0) | (4 if "nocluster" in sys.argv[3:] else 0)
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
 crs_mode = "crs" in sys.argv[3:]
 if crs_mode:

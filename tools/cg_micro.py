@@ -1,7 +1,7 @@
 """CG kernel microbenchmark: fixed-iteration Jacobi-PCG on a cavity
 Laplacian-like SPD matrix (K = 7) through fvb_op_cg; prints device time per
 iteration and the algorithmic HBM rate (N(12K+96) bytes per iteration).
-Usage: python tools/cg_micro.py N ITERS [crs|perm] [explicit] [norcm]
+Usage: python tools/cg_micro.py N ITERS [crs|perm] [explicit] [norcm] [nocluster] [grid=B]
 "crs" adds long-range couplings: CRS tail + escaped stencil-code rows; "perm"
 randomly renumbers the box: no stencil codes, RCM-ordered solve; "explicit"
 and "norcm" set the context's solver format options (fvb_set_solver_options:
@@ -15,7 +15,8 @@ from paper_1207_1571_b200 import _lib, cases, sparse
 from paper_1207_1571_b200.device import context_for
 
 n = int(sys.argv[1]); iters = int(sys.argv[2])
-opts = (1 if "explicit" in sys.argv[3:] else 0) | (2 if "norcm" in sys.argv[3:] else 0)
+opts = (1 if "explicit" in sys.argv[3:] else 0) | (2 if "norcm" in sys.argv[3:] else 0) | \
+    (4 if "nocluster" in sys.argv[3:] else 0)
 t0 = time.time()
 mesh = cases.box_mesh(n, n, n, 1.0, 1.0, 1.0, [("all", "wall", ["x-", "x+", "y-", "y+", "z-", "z+"])])
 if len(sys.argv) > 3 and sys.argv[3] == "perm":

@@ -16,11 +16,22 @@ case = Case("c1", m, cc)
 cfg = CouplingConfig.from_case_config(cc)
 st = init_state(case, cfg)
 piso_time_step(st, cfg)
+import ctypes as C
+from paper_1207_1571_b200 import _lib
+h = st._ctx.h
 t0 = time.perf_counter()
+ccall = 0.0
+_lib.check(_lib.lib.fvb_timer_start(h))
 for _ in range(99):
     piso_time_step(st, cfg)
+    ccall += st._last_step_s
+dev = C.c_double()
+_lib.check(_lib.lib.fvb_timer_stop(h, C.byref(dev)))
 dt = (time.perf_counter() - t0) / 99
+# wall per step, of which inside the C call (host launches + syncs), and the
+# device time between the first and last event of the 99 steps
 print(json.dumps({"case": "C1 cavity 20x20x1 PISO", "ms_per_step": 1e3 * dt,
+                  "c_call_ms_per_step": 1e3 * ccall / 99, "device_span_ms_per_step": dev.value / 99,
                   "cg_iters_per_step": st.cum_iters["cg"] / 100, "reference_ms_per_step": 7.4}))
 case = cases.gen_backward_step(16)
 cfg = CouplingConfig.from_case_config(case.config)
