@@ -309,6 +309,10 @@ constexpr size_t kStepPartials = 32768;
 // single-domain systems up to this many rows solve on one thread-block
 // cluster (cluster_reduce), larger ones on the full persistent grid
 constexpr int kClusterMaxRows = 40000;
+// ... and systems of at most this many rows per thread of one block run on a
+// single block (block barriers; tools/cg_micro.py: CG at 3375 rows 9.4 us
+// per iteration on one block against ~7 on a 16-CTA cluster)
+constexpr int kSingleBlockRowsPerThread = 2;
 constexpr size_t kResults = 16 * 4096;
 
 // ------------------------------------------------------- kernel helpers
@@ -538,10 +542,17 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[M], double* smem, uns
   }
   cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
   cl.sync();
+  // remote loads in parallel (one value per thread), then the rank-order sum
+  const unsigned nb = cl.num_blocks();
+  __shared__ double s_all[16 * kRedStride];
+  if (threadIdx.x < nb * unsigned(M)) {
+    const unsigned b = threadIdx.x / unsigned(M), m = threadIdx.x % unsigned(M);
+    s_all[b * M + m] = cl.map_shared_rank(mine, b)[m];
+  }
+  __syncthreads();
   if (threadIdx.x < unsigned(M)) {
-    const unsigned nb = cl.num_blocks();
     double acc = 0.0;
-    for (unsigned b = 0; b < nb; ++b) acc += cl.map_shared_rank(mine, b)[threadIdx.x];
+    for (unsigned b = 0; b < nb; ++b) acc += s_all[b * M + threadIdx.x];
     smem[32 * M + threadIdx.x] = acc;
   }
   __syncthreads();

@@ -963,8 +963,9 @@ int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   const int share = c->sm_share > 0 ? c->sm_share : 1;
   int b = share > 1 ? per_sm * (c->num_sms - share) / share : per_sm * c->num_sms;
   // small systems: one block (block barriers instead of grid barriers) while
-  // the rows per thread stay low
-  if (!c->teamed() && c->nr <= 4 * threads) b = 1;
+  // a block holds at most two rows per thread (larger ones up to
+  // kClusterMaxRows run as one cluster, cluster_want)
+  if (!c->teamed() && c->nr <= kSingleBlockRowsPerThread * threads) b = 1;
   if (c->solver_max_blocks > 0 && b > c->solver_max_blocks) b = c->solver_max_blocks;
   if (b > int(kStepPartials / (2 * kRedStride))) b = int(kStepPartials / (2 * kRedStride));
   *blocks = b < 1 ? 1 : b;
@@ -1040,15 +1041,15 @@ int cluster_launch(Ctx* c, K kernel, Args& args, int threads, int blocks) {
 }
 
 // cluster size for a single-domain solve of nr rows with `threads`-thread
-// CTAs: about two rows per thread, at least 2 CTAs, none when the system is
+// CTAs: the largest cluster the device co-schedules (16), none when the system is
 // large (the full grid wins above ~40k rows, tools/cg_micro.py) or fits one
 // block (block barriers), or the context asks for the grid path
 inline int cluster_want(const Ctx* c, int threads) {
   if (c->teamed() || (c->solver_flags & FVB_SOLVER_NO_CLUSTER) || c->sm_share > 1) return 0;
-  if (c->nr <= 4 * threads || c->nr > kClusterMaxRows) return 0;
+  if (c->nr <= kSingleBlockRowsPerThread * threads || c->nr > kClusterMaxRows) return 0;
   if (c->solver_max_blocks > 0) return 0;  // an explicit grid cap wins
-  int b = (c->nr + 2 * threads - 1) / (2 * threads);
-  return b < 2 ? 2 : (b > 16 ? 16 : b);
+  (void)threads;
+  return 16;  // as many SMs as one cluster can hold (cluster_blocks clamps)
 }
 
 // Inverse diagonal of the owned rows, and the first zero-diagonal row into
