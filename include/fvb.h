@@ -334,7 +334,7 @@ int fvb_set_sm_share(fvb_ctx* ctx, int share);
  * Used by the format-equivalence tests and tools/cg_micro.py. */
 #define FVB_SOLVER_EXPLICIT_INDEX 1 /* SpMV passes read int32 indices, not stencil codes */
 #define FVB_SOLVER_NO_RCM 2         /* solve in the mesh order on renumbered meshes */
-#define FVB_SOLVER_NO_CLUSTER 4     /* small systems on the grid, not one thread-block cluster */
+#define FVB_SOLVER_NO_CLUSTER 4     /* small systems on the plain grid / block path (no one-cluster or shared-memory solver) */
 int fvb_set_solver_options(fvb_ctx* ctx, int flags);
 
 /* grid of the persistent solver kernels (no reference counterpart): at most

@@ -240,8 +240,8 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
 // L2-only loads; KT = 0: generic K, plain row loops.  Rows are grid-strided
 // over every thread (team_rows).
 template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false,
-          bool CLUSTER = false>
-__global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
+          bool CLUSTER = false, bool SMEM = false>
+__device__ __forceinline__ void cg_body(const CgParams& A) {
   __shared__ double red[32 * 3 + 3];
   // SC: stencil-coded pass A (PatternView::code) with the code table here
   __shared__ int s_tab[SC ? kMaxCodes * (KT > 0 ? KT : 1) : 1];
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     __syncthreads();
   }
   if (zero_diag_exit(A.zero_flag, A.result, 1)) return;
-  constexpr bool PB2 = KT > 0;
+  constexpr bool PB2 = KT > 0 && !SMEM;  // 16-byte global loads: not on shared memory
   const PatternView& P = A.P;
   const TeamView& T = A.T;
   const int nrows = P.n;
@@ -424,6 +424,32 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   }
 }
 
+// Persistent CG kernel.  SMEM (single-block systems, one block): the work
+// vectors r, z, the two p buffers, q and 1/D live in dynamic shared memory
+// for the whole solve, so the gathers of pass A are shared-memory loads
+// (x, b and the matrix stay in global memory: own-row or streamed accesses).
+template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false,
+          bool CLUSTER = false, bool SMEM = false>
+__global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
+  if constexpr (SMEM) {
+    extern __shared__ double dyn[];
+    const int n = A.P.n;
+    CgParams B = A;
+    B.r = dyn;
+    B.z = dyn + n;
+    B.pa = dyn + 2 * n;
+    B.pb = dyn + 3 * n;
+    B.q = dyn + 4 * n;
+    double* inv = dyn + 5 * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) inv[i] = A.inv[i];
+    B.inv = inv;
+    __syncthreads();
+    cg_body<KT, THREADS, MINB, SC, DF, TEAM, CLUSTER, true>(B);
+  } else {
+    cg_body<KT, THREADS, MINB, SC, DF, TEAM, CLUSTER, false>(A);
+  }
+}
+
 // ------------------------------------------------------------ BiCGStab
 // y_c = A x_c for NC vectors sharing one pass over V and I.
 template <int KT, int NC, typename G>
@@ -594,8 +620,9 @@ struct Bi3Params {
 #define FVB_BI_MINB 2
 #endif
 
-template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false>
-__global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Params<NC> A) {
+template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false,
+          bool SMEM = false>
+__device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
   __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
   __shared__ CompState S[NC];
   // SC: stencil-coded SpMV sweeps (PatternView::code) with the code table here
@@ -628,7 +655,7 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
              reinterpret_cast<uintptr_t>(A.rh[c]) | reinterpret_cast<uintptr_t>(A.t[c]) |
              reinterpret_cast<uintptr_t>(A.p[0][c]) | reinterpret_cast<uintptr_t>(A.p[1][c]) |
              reinterpret_cast<uintptr_t>(A.v[0][c]) | reinterpret_cast<uintptr_t>(A.v[1][c]);
-  const bool vec_ok = (al_or & 15u) == 0;
+  const bool vec_ok = !SMEM && (al_or & 15u) == 0;  // 16-byte global loads
 
   // setup (linsolve.py:180-196): r = b - A x0, r_hat = r, ||b||, ||r||
   double sums[2 * NC];
@@ -949,6 +976,51 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
   }
 }
 
+// Persistent batched BiCGStab.  SMEM (single-block systems): r, r_hat, the
+// p / d and v buffers, t and 1/D live in dynamic shared memory for the
+// solve (x and b stay in global memory).
+template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false,
+          bool SMEM = false>
+__global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Params<NC> A) {
+  if constexpr (SMEM) {
+    extern __shared__ double dyn[];
+    const int n = A.P.n;
+    Bi3Params<NC> B = A;
+    double* q = dyn;
+    for (int c = 0; c < NC; ++c) {
+      B.r[c] = q; q += n;
+      B.rh[c] = q; q += n;
+      B.p[0][c] = q; q += n;
+      B.p[1][c] = q; q += n;
+      B.v[0][c] = q; q += n;
+      B.v[1][c] = q; q += n;
+      B.t[c] = q; q += n;
+    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) q[i] = A.inv[i];
+    B.inv = q;
+    __syncthreads();
+    bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, true>(B);
+  } else {
+    bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, false>(A);
+  }
+}
+
+// dynamic shared memory of the SMEM solver kernels for n rows (0 = too large)
+inline size_t smem_cg_bytes(int n) { return size_t(6) * n * sizeof(double); }
+inline size_t smem_bi_bytes(int n, int nc) { return size_t(7 * nc + 1) * n * sizeof(double); }
+constexpr size_t kSmemSolverMax = 200 * 1024;
+
+template <typename K, typename Args>
+int smem_launch(Ctx* c, K kernel, Args& args, int threads, size_t bytes) {
+  FVB_CUDA(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(bytes)));
+  FVB_CUDA(cudaMemsetAsync(c->sync, 0, 3 * sizeof(unsigned), c->stream));
+  void* params[] = {&args};
+  fvb::note_launch();
+  FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(1), dim3(threads), params, bytes, c->stream));
+  return FVB_OK;
+}
+
 template <typename K>
 int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   int per_sm = 0;
@@ -1164,6 +1236,15 @@ __global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ pe
 // deferred x update on 7-point rows, team or single domain
 template <bool TEAM>
 static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
+  if (!TEAM && (c->k == 7 || c->k == 5) && c->nr <= kSingleBlockRowsPerThread * 1024 &&
+      smem_cg_bytes(c->nr) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
+    const size_t bytes = smem_cg_bytes(c->nr);
+    if (c->k == 7)
+      return sc ? smem_launch(c, k_cg<7, 1024, 1, 1, 1, false, false, true>, prm, 1024, bytes)
+                : smem_launch(c, k_cg<7, 1024, 1, 0, 1, false, false, true>, prm, 1024, bytes);
+    return sc ? smem_launch(c, k_cg<5, 1024, 1, 1, 0, false, false, true>, prm, 1024, bytes)
+              : smem_launch(c, k_cg<5, 1024, 1, 0, 0, false, false, true>, prm, 1024, bytes);
+  }
   if (!TEAM && (c->k == 7 || c->k == 5)) {
     const int want = cluster_want(c, 1024);
     const int nb = want ? (c->k == 7 ? cluster_blocks(c, k_cg<7, 1024, 1, 1, 1, false, true>, 1024, want)
@@ -1324,6 +1405,15 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
                         : coop_launch(c, k_bicgstab3<7, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
       default: return coop_launch(c, k_bicgstab3<0, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
     }
+  }
+  if ((c->k == 7 || c->k == 5) && !pov && c->nr <= kSingleBlockRowsPerThread * kSolverThreads &&
+      smem_bi_bytes(c->nr, NC) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
+    const size_t bytes = smem_bi_bytes(c->nr, NC);
+    if (c->k == 7)
+      return sc ? smem_launch(c, k_bicgstab3<7, NC, true, false, false, true>, prm, kSolverThreads, bytes)
+                : smem_launch(c, k_bicgstab3<7, NC, false, false, false, true>, prm, kSolverThreads, bytes);
+    return sc ? smem_launch(c, k_bicgstab3<5, NC, true, false, false, true>, prm, kSolverThreads, bytes)
+              : smem_launch(c, k_bicgstab3<5, NC, false, false, false, true>, prm, kSolverThreads, bytes);
   }
   if (c->k == 7 || c->k == 5) {
     const int want = cluster_want(c, kSolverThreads);
