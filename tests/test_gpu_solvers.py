@@ -328,3 +328,45 @@ def test_rcm_ordered_bicgstab_single_and_batched():
         assert np.linalg.norm(B[:, c] - M @ x1) <= 1e-8 * np.linalg.norm(B[:, c])
     _lib.check(_lib.lib.fvb_pattern_codes(ctx.h, None, None, None, C.byref(r1c)))
     assert r1c.value - r0.value == 4  # one batch + three single solves
+
+
+@pytest.mark.parametrize("n", [7, 20])
+def test_small_system_paths_match_grid_path(n):
+    # n=7 (343 rows): one block with the work vectors in shared memory;
+    # n=20 (8000 rows): one 16-CTA thread-block cluster (DSMEM reductions).
+    # Both against the plain block / grid path (FVB_SOLVER_NO_CLUSTER): same
+    # row arithmetic, only the grouping of the dot products differs.
+    from paper_1207_1571_b200 import _lib
+    from paper_1207_1571_b200.device import context_for
+
+    rng = np.random.default_rng(40 + n)
+    p, A, M = _box_operator(n, False, rng)
+    N = p.n
+    b = rng.normal(size=N)
+    B = rng.normal(size=(N, 3))
+    # SPD copy for CG: symmetric part made diagonally dominant
+    S = sparse.HybridMatrix.zeros(p)
+    rows = np.arange(N)[:, None]
+    S.V[:] = np.where(p.I >= 0, -1.0, 0.0)
+    S.V[np.arange(N), p.diag_slot] = (p.I >= 0).sum(axis=1) - 1 + 0.05
+    cfg = SolveConfig(tolerance=1e-11, max_iters=5000)
+    ctx = context_for(None, None, p)
+    out = {}
+    for mode, flags in (("small", 0), ("grid", _lib.SOLVER_NO_CLUSTER)):
+        _lib.check(_lib.lib.fvb_set_solver_options(ctx.h, flags))
+        try:
+            out[mode] = (cg(S, b, np.zeros(N), cfg), bicgstab_batched(A, B, np.zeros((N, 3)), cfg))
+        finally:
+            _lib.check(_lib.lib.fvb_set_solver_options(ctx.h, 0))
+    (xs, rs), (Xs, Rs) = out["small"]
+    (xg, rg), (Xg, Rg) = out["grid"]
+    assert rs.converged and rg.converged and abs(rs.iterations - rg.iterations) <= 1
+    assert rel(xs, xg) < 1e-9
+    for c in range(3):
+        assert Rs[c].converged and abs(Rs[c].iterations - Rg[c].iterations) <= 2
+        assert rel(Xs[:, c], Xg[:, c]) < 1e-8
+        assert np.linalg.norm(B[:, c] - M @ Xs[:, c]) <= 1e-9 * np.linalg.norm(B[:, c])
+    # deterministic: a repeat of the small-path solves is bitwise equal
+    x2, r2 = cg(S, b, np.zeros(N), cfg)
+    X2, R2 = bicgstab_batched(A, B, np.zeros((N, 3)), cfg)
+    assert np.array_equal(x2, xs) and np.array_equal(X2, Xs)

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+for n in 5 7 10; do echo "cg n=$n $(timeout 120 python tools/cg_micro.py $n 300 | cut -c1-170)"; done
+for n in 7 10; do echo "bi n=$n $(timeout 120 python tools/bi_micro.py $n 60 | cut -c1-170)"; done
+timeout 300 python tools/small_bench.py
+timeout 900 python tools/bicgstab_diag.py c4 > gpurun_out/r02t_bidiag_c4.log 2>&1; cat gpurun_out/r02t_bidiag_c4.log
+timeout 900 python -m pytest tests/test_gpu_solvers.py tests/test_gpu_configs.py -q -rf 2>&1 | tail -3
