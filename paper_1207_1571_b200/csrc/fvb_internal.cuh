@@ -564,7 +564,9 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[M], double* smem, uns
 // TEAM = false: the kernel instantiation for a single domain, which
 // compiles the team path away (it costs registers in the solver loops).
 // CLUSTER: the kernel runs as one thread-block cluster (cluster_reduce).
-template <int M, bool OOL = false, bool TEAM = true, bool CLUSTER = false>
+// SYS: a team over several devices (compile-time, so the single-device and
+// co-resident team kernels carry no system-scope code).
+template <int M, bool OOL = false, bool TEAM = true, bool CLUSTER = false, bool SYS = false>
 __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
                                             double* smem /*[32*M+M]*/, unsigned& rnd,
@@ -621,13 +623,12 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
           break;
         }
       }
-      // acquire before anyone reads partials or vectors of other blocks.
-      // The load's value must be used: ptxas drops an ld.acquire whose
-      // result is discarded and keeps only its L1 invalidate, which left
-      // the relaxed polls above as the only synchronisation — a 1-in-100
-      // run-to-run difference in the 128^3 stress (profiles/r02_stress.md).
-      while (ld_acquire_gpu(sync) < target && *vabort == 0) {
-      }
+      // acquire before anyone reads partials or vectors of other blocks:
+      // the relaxed load that observed every arrival + fence.acq_rel is an
+      // acquire pattern (and invalidates this SM's L1).  (An ld.acquire
+      // whose value is unused is dropped by ptxas down to its L1
+      // invalidate, which is what round 1 had.)
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
       s_ok = *vabort == 0;
     }
     __syncthreads();
@@ -655,15 +656,15 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
   // sys: the peers are other devices, so arrivals order this block's halo
   // stores at system scope
   const bool teamed = T.size > 1;
-  // Multi-device team (T.sys): every block fences at system scope before its
-  // arrival, so its halo stores to the peers (NVLink) are ordered before the
-  // last arriver's mailbox flags by the storing block itself — not only
-  // through the cumulativity of the last arriver's fence.sc.sys, which a
-  // bare gpu-scope arrival would rely on.  One device (all
+  // Multi-device team (SYS kernels): every block's arrival is a system-scope
+  // acq_rel atomic, so its halo stores to the peers (NVLink) are ordered
+  // before the last arriver's mailbox flags by the storing block itself —
+  // not only through the cumulativity of the last arriver's fence.sc.sys,
+  // which a gpu-scope arrival would rely on.  One device (all
   // ranks co-resident, tests): gpu scope.  (A gpu-scope arrival measured
   // ~6 us less per reduction on one device, profiles/r01_team.md, but a
   // multi-GPU run has not validated it.)
-  const bool sys = teamed && T.sys && sends;
+  (void)sends;  // every block of a team holds send rows (grid-strided rows)
   block_reduce<M>(v, smem);
   volatile unsigned* vabort = sync + 2;
   double* bcast = reinterpret_cast<double*>(sync + 4);
@@ -676,8 +677,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     double* part = partials + size_t(gen & 1u) * kRedStride * gridDim.x;
 #pragma unroll
     for (int m = 0; m < M; ++m) part[size_t(m) * gridDim.x + blockIdx.x] = v[m];
-    if (sys) __threadfence_system();  // (a predicated fence: no second atomic form)
-    s_last = atom_arrive(sync, false) == gridDim.x - 1;
+    s_last = atom_arrive(sync, SYS) == gridDim.x - 1;  // system scope in a multi-device team
   }
   __syncthreads();
   const unsigned gen = s_gen;
@@ -721,9 +721,10 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     }
   }
   if (threadIdx.x == 0) {
-    // acquire (value used, see the single-device path) before reading results
-    while (ld_acquire_gpu(sync + 1) == gen && *vabort == 0) {
-    }
+    // acquire before reading results: the relaxed load that observed the
+    // new generation (or the last arriver's own release) + fence.acq_rel
+    // is an acquire pattern (and invalidates this SM's L1)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
     s_ok = *vabort == 0;
     if (teamed) {
 #pragma unroll

@@ -211,18 +211,24 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
         ci[s] = c < 0 ? 0 : c;
       }
     }
-    // issue every gather of the row before the first use (memory-level
-    // parallelism: the compiler otherwise interleaves load-use pairs)
-    double zg[KT], pg[KT];
-#pragma unroll
-    for (int s = 0; s < KT; ++s) zg[s] = z[ci[s]];
-    if (!first) {
-#pragma unroll
-      for (int s = 0; s < KT; ++s) pg[s] = po[ci[s]];
-    }
     double pr[KT];
+    if constexpr (!TEAM) {
+      // issue every gather of the row before the first use (memory-level
+      // parallelism: the compiler otherwise interleaves load-use pairs);
+      // the team kernel has no registers to spare for it
+      double zg[KT], pg[KT];
 #pragma unroll
-    for (int s = 0; s < KT; ++s) pr[s] = vi[s] * (first ? zg[s] : pg[s] * beta + zg[s]);
+      for (int s = 0; s < KT; ++s) zg[s] = z[ci[s]];
+      if (!first) {
+#pragma unroll
+        for (int s = 0; s < KT; ++s) pg[s] = po[ci[s]];
+      }
+#pragma unroll
+      for (int s = 0; s < KT; ++s) pr[s] = vi[s] * (first ? zg[s] : pg[s] * beta + zg[s]);
+    } else {
+#pragma unroll
+      for (int s = 0; s < KT; ++s) pr[s] = vi[s] * g(ci[s]);
+    }
     double ev = pr[0];
 #pragma unroll
     for (int s = 2; s < KT; s += 2) ev = ev + pr[s];
@@ -251,7 +257,7 @@ __device__ __forceinline__ double cg_pass_a_codes(const CgParams& A, const doubl
 // L2-only loads; KT = 0: generic K, plain row loops.  Rows are grid-strided
 // over every thread (team_rows).
 template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false,
-          bool CLUSTER = false, bool SMEM = false>
+          bool CLUSTER = false, bool SMEM = false, bool SYS = false>
 __device__ __forceinline__ void cg_body(const CgParams& A) {
   __shared__ double red[32 * 3 + 3];
   // SC: stencil-coded pass A (PatternView::code) with the code table here
@@ -295,7 +301,7 @@ __device__ __forceinline__ void cg_body(const CgParams& A) {
       s3[2] += ri * zi;
     }
   }
-  if (!team_reduce<3, true, TEAM, CLUSTER>(T, A.sync, A.partials, s3, red, rnd, sends)) {
+  if (!team_reduce<3, true, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, s3, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0) A.result[4] = SE_TIMEOUT;
     return;
   }
@@ -350,7 +356,7 @@ __device__ __forceinline__ void cg_body(const CgParams& A) {
     }
     if (DEFER) p_pend = nullptr;  // pass A applied the previous update
     if (timer) { const uint64_t t = global_ns(); t_spmv += t - tk; tk = t; }
-    if (!team_reduce<1, true, TEAM, CLUSTER>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<1, true, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, pq, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) { const uint64_t t = global_ns(); t_red += t - tk; tk = t; }
     if (pq[0] <= 0.0 || !isfinite(pq[0])) { err = SE_CG_NOT_SPD; break; }
     const double alpha = rz / pq[0];
@@ -407,7 +413,7 @@ __device__ __forceinline__ void cg_body(const CgParams& A) {
       p_pend = pnew;
       alpha_prev = alpha;
     }
-    if (!team_reduce<2, true, TEAM, CLUSTER>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
+    if (!team_reduce<2, true, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, s2, red, rnd, sends)) { err = SE_TIMEOUT; break; }
     if (timer) t_red += global_ns() - tk;
     res = sqrt(s2[0]) / bnorm;
     if (!isfinite(res)) { err = SE_DIVERGED; break; }
@@ -440,7 +446,7 @@ __device__ __forceinline__ void cg_body(const CgParams& A) {
 // for the whole solve, so the gathers of pass A are shared-memory loads
 // (x, b and the matrix stay in global memory: own-row or streamed accesses).
 template <int KT, int THREADS, int MINB, int SC = 0, int DF = 0, bool TEAM = false,
-          bool CLUSTER = false, bool SMEM = false>
+          bool CLUSTER = false, bool SMEM = false, bool SYS = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
   if constexpr (SMEM) {
     extern __shared__ double dyn[];
@@ -466,7 +472,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_cg(CgParams A) {
     __syncthreads();
     cg_body<KT, THREADS, MINB, SC, DF, TEAM, CLUSTER, true>(B);
   } else {
-    cg_body<KT, THREADS, MINB, SC, DF, TEAM, CLUSTER, false>(A);
+    cg_body<KT, THREADS, MINB, SC, DF, TEAM, CLUSTER, false, SYS>(A);
   }
 }
 
@@ -644,7 +650,7 @@ struct Bi3Params {
 #endif
 
 template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false,
-          bool SMEM = false>
+          bool SMEM = false, bool SYS = false>
 __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
   __shared__ double red[32 * 3 * NC + 3 * NC];  // team_reduce<3 NC> in pass 2
   __shared__ CompState S[NC];
@@ -705,7 +711,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
       }
     }
   }
-  if (!team_reduce<2 * NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, sums, red, rnd, sends)) {
+  if (!team_reduce<2 * NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, sums, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
@@ -814,7 +820,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -861,7 +867,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<3 * NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<3 * NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -968,7 +974,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC, false, TEAM, CLUSTER>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -1003,7 +1009,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
 // p / d and v buffers, t and 1/D live in dynamic shared memory for the
 // solve (x and b stay in global memory).
 template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false,
-          bool SMEM = false>
+          bool SMEM = false, bool SYS = false>
 __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Params<NC> A) {
   if constexpr (SMEM) {
     extern __shared__ double dyn[];
@@ -1035,7 +1041,7 @@ __global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Pa
     __syncthreads();
     bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, true>(B);
   } else {
-    bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, false>(A);
+    bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, false, SYS>(A);
   }
 }
 
@@ -1275,7 +1281,7 @@ __global__ void k_rcm_scatter_multi(int n, int ncomp, const int* __restrict__ pe
 
 // k_cg instantiation for the context: K (5, 7 or generic), stencil codes,
 // deferred x update on 7-point rows, team or single domain
-template <bool TEAM>
+template <bool TEAM, bool SYS = false>
 static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
   if (!TEAM && (c->k == 7 || c->k == 5) && c->nr <= kSingleBlockRowsPerThread * 1024 &&
       smem_cg_bytes(c->nr, c->k) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
@@ -1301,12 +1307,12 @@ static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
   }
   switch (c->k) {
     case 5:
-      if (sc) return coop_launch(c, k_cg<5, 1024, 1, 1, 0, TEAM>, prm, 1024, 1);
-      return coop_launch(c, k_cg<5, 1024, 1, 0, 0, TEAM>, prm, 1024, 1);
+      if (sc) return coop_launch(c, k_cg<5, 1024, 1, 1, 0, TEAM, false, false, SYS>, prm, 1024, 1);
+      return coop_launch(c, k_cg<5, 1024, 1, 0, 0, TEAM, false, false, SYS>, prm, 1024, 1);
     case 7:  // x update folded into pass A (cg_defers_x)
-      if (sc) return coop_launch(c, k_cg<7, 1024, 1, 1, 1, TEAM>, prm, 1024, 1);
-      return coop_launch(c, k_cg<7, 1024, 1, 0, 1, TEAM>, prm, 1024, 1);
-    default: return coop_launch(c, k_cg<0, 512, 2, 0, 0, TEAM>, prm);
+      if (sc) return coop_launch(c, k_cg<7, 1024, 1, 1, 1, TEAM, false, false, SYS>, prm, 1024, 1);
+      return coop_launch(c, k_cg<7, 1024, 1, 0, 1, TEAM, false, false, SYS>, prm, 1024, 1);
+    default: return coop_launch(c, k_cg<0, 512, 2, 0, 0, TEAM, false, false, SYS>, prm);
   }
 }
 
@@ -1368,8 +1374,10 @@ int cg_solve(Ctx* c, MatView A, const double* b, double* x, double tol, double a
   // pattern has them, else on the explicit index ring (tuning history:
   // profiles/r01_cg_variants.md)
   const bool sc = uses_codes(c);
-  if (c->teamed())
-    FVB_TRY(cg_launch<true>(c, prm, sc));
+  if (c->teamed() && c->team.sys)
+    FVB_TRY((cg_launch<true, true>(c, prm, sc)));
+  else if (c->teamed())
+    FVB_TRY((cg_launch<true, false>(c, prm, sc)));
   else
     FVB_TRY(cg_launch<false>(c, prm, sc));
   if (rcm) {
@@ -1440,6 +1448,15 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   // stencil-coded SpMV sweeps when the pattern has codes (unless the
   // context asks for the explicit indices, FVB_SOLVER_EXPLICIT_INDEX)
   const bool sc = uses_codes(c);
+  if (c->teamed() && c->team.sys) {
+    switch (c->k) {
+      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB)
+                        : coop_launch(c, k_bicgstab3<5, NC, false, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB)
+                        : coop_launch(c, k_bicgstab3<7, NC, false, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+      default: return coop_launch(c, k_bicgstab3<0, NC, false, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+    }
+  }
   if (c->teamed()) {
     switch (c->k) {
       case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true>, prm, kSolverThreads, FVB_BI_MINB)
