@@ -387,6 +387,34 @@ __device__ __forceinline__ void block_reduce(double (&v)[M], double* smem /*[32*
   __syncthreads();
 }
 
+// block_reduce without the trailing barrier (result in thread 0): for the
+// single-block and cluster reductions, whose next barrier already orders
+// the reuse of smem
+template <int M>
+__device__ __forceinline__ void block_reduce_lean(double (&v)[M], double* smem /*[32*M]*/) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int m = 0; m < M; ++m) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[m] += __shfl_down_sync(0xffffffffu, v[m], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) smem[warp * M + m] = v[m];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      double x = lane < nw ? smem[lane * M + m] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      v[m] = x;
+    }
+  }
+}
+
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -533,7 +561,7 @@ constexpr size_t kRedStride = 16;
 template <int M>
 __device__ __forceinline__ void cluster_reduce(double (&v)[M], double* smem, unsigned& rnd) {
   __shared__ double s_cl[2][kRedStride];
-  block_reduce<M>(v, smem);
+  block_reduce_lean<M>(v, smem);
   double* mine = s_cl[rnd & 1u];
   ++rnd;
   if (threadIdx.x == 0) {
@@ -558,7 +586,8 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[M], double* smem, uns
   __syncthreads();
 #pragma unroll
   for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
-  __syncthreads();
+  // (no trailing barrier: the next reduction's cluster barrier orders the
+  // reuse of smem and s_all)
 }
 
 // TEAM = false: the kernel instantiation for a single domain, which
@@ -582,7 +611,9 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
 #ifdef FVB_DIAG_FENCE  // diagnostic build (tools/build_variant.py): every thread fences
   __threadfence();
 #endif
-  if (!TEAM || T.size <= 1) {
+  // (TEAM kernels are launched for decomposed meshes only: no single-device
+  // path in them)
+  if (!TEAM) {
     // One device: a monotonic arrival counter, no last-arriver hand-off.
     // Every block publishes its partials, arrives with a release add and
     // waits until all gridDim.x blocks of round rnd arrived, then sums the
@@ -591,9 +622,11 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     // r+2 only after passing round r+1, i.e. after every block finished
     // reading round r.
     (void)sends;
-    block_reduce<M>(v, smem);
     if (gridDim.x == 1) {
-      // small systems run on a single block: the block barrier is the grid barrier
+      // small systems run on a single block: the block barrier is the grid
+      // barrier (two barriers per reduction: the next reduction's first one
+      // orders the reuse of the broadcast slot)
+      block_reduce_lean<M>(v, smem);
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int m = 0; m < M; ++m) smem[32 * M + m] = v[m];
@@ -601,10 +634,10 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
       __syncthreads();
 #pragma unroll
       for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
-      __syncthreads();
       ++rnd;
       return true;
     }
+    block_reduce<M>(v, smem);
     const unsigned r = rnd++;
     double* part = partials + size_t(r & 1u) * kRedStride * gridDim.x;
     volatile unsigned* vabort = sync + 2;
