@@ -63,7 +63,7 @@ use_codes = codes.value > 0
 # the two SpMV passes read 1-byte stencil codes instead of K int32 indices
 row_bytes = 600.0 - (2 * (4 * K - 1) if use_codes else 0)
 it = reps[0].iterations
-print(json.dumps({"options": opts, "n": n, "k": int(K),
+print(json.dumps({"options": opts, "res_full": [reps[c].final_residual for c in range(3)], "n": n, "k": int(K),
                   "nnz_crs": int(pat.nnz_crs),
                   "iters": [reps[c].iterations for c in range(3)],
                   "err": [reps[c].error_kind for c in range(3)] if hasattr(reps[0], "error_kind") else None,
