@@ -787,7 +787,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
 }
 
 // ------------------------------------------------------------ launchers
-// (implemented in fvb_ops.cu / fvb_solvers.cu / fvb_team.cu)
+// (implemented in fvb_ops.cu / fvb_cg.cu / fvb_bicgstab.cu / fvb_team.cu)
 int launch_inv_diag(Ctx* c, const double* V, double* inv, int* first_zero);
 int smvp(Ctx* c, MatView A, const double* x, double* y);
 int stmvp(Ctx* c, MatView A, const int* J, const int* twin_crs, const uint8_t* ct_in_ell,
