@@ -123,3 +123,24 @@ def test_ipc_team_two_processes_one_device():
     ta = [int(x) for x in team.split(",")]
     sa = [int(x) for x in single.split(",")]
     assert len(ta) == len(sa) and all(abs(a - b) <= 1 for a, b in zip(ta, sa)), line[0]
+
+
+@pytest.mark.parametrize("nparts", [2, 4])
+def test_team_system_scope_kernels(nparts, monkeypatch):
+    # the kernels a team over several GPUs uses (system-scope arrivals and
+    # mailbox fences, the SYS instantiations), forced on one device with
+    # FVB_TEAM_SCOPE=sys: same results as the single-domain run under the
+    # parity rules
+    monkeypatch.setenv("FVB_TEAM_SCOPE", "sys")
+    case = cases.gen_cavity(12)
+    case.config.algorithm, case.config.dt = "piso", 0.1 / 12
+    case.config.cg_tol, case.config.bicgstab_tol, case.config.max_iters = 1e-13, 1e-10, 20000
+    cfg = CouplingConfig.from_case_config(case.config)
+    st = _single(case, cfg, 2)
+    run = _team(case, cfg, 2, nparts)
+    u, p, flux = run.gather()
+    assert rel(u, st.u.values) < 1e-9 and rel(p, st.p.values) < 1e-9 and rel(flux, st.flux) < 1e-9
+    for a, b in zip(run.residual_log, st.residual_log):
+        assert abs(a[3] - b[3]) <= (2 if a[0] == "cg" else 3), (a, b)
+    assert run.continuity_error() <= 1e-8 * np.abs(flux).max()
+    run.close()
