@@ -177,9 +177,7 @@ struct Bi3Params {
 };
 
 // resident 512-thread blocks per SM of the BiCGStab kernel (64 registers)
-#ifndef FVB_BI_MINB
-#define FVB_BI_MINB 2
-#endif
+constexpr int kBiBlocksPerSM = 2;
 
 template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false,
           bool SMEM = false, bool SYS = false>
@@ -542,7 +540,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
 // solve (x and b stay in global memory).
 template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = false,
           bool SMEM = false, bool SYS = false>
-__global__ void __launch_bounds__(kSolverThreads, FVB_BI_MINB) k_bicgstab3(Bi3Params<NC> A) {
+__global__ void __launch_bounds__(kSolverThreads, kBiBlocksPerSM) k_bicgstab3(Bi3Params<NC> A) {
   if constexpr (SMEM) {
     extern __shared__ double dyn[];
     const int n = A.P.n;
@@ -648,20 +646,20 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   const bool sc = uses_codes(c);
   if (c->teamed() && c->team.sys) {
     switch (c->k) {
-      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB)
-                        : coop_launch(c, k_bicgstab3<5, NC, false, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB);
-      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB)
-                        : coop_launch(c, k_bicgstab3<7, NC, false, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB);
-      default: return coop_launch(c, k_bicgstab3<0, NC, false, true, false, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true, false, false, true>, prm, kSolverThreads, kBiBlocksPerSM)
+                        : coop_launch(c, k_bicgstab3<5, NC, false, true, false, false, true>, prm, kSolverThreads, kBiBlocksPerSM);
+      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true, false, false, true>, prm, kSolverThreads, kBiBlocksPerSM)
+                        : coop_launch(c, k_bicgstab3<7, NC, false, true, false, false, true>, prm, kSolverThreads, kBiBlocksPerSM);
+      default: return coop_launch(c, k_bicgstab3<0, NC, false, true, false, false, true>, prm, kSolverThreads, kBiBlocksPerSM);
     }
   }
   if (c->teamed()) {
     switch (c->k) {
-      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true>, prm, kSolverThreads, FVB_BI_MINB)
-                        : coop_launch(c, k_bicgstab3<5, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
-      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true>, prm, kSolverThreads, FVB_BI_MINB)
-                        : coop_launch(c, k_bicgstab3<7, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
-      default: return coop_launch(c, k_bicgstab3<0, NC, false, true>, prm, kSolverThreads, FVB_BI_MINB);
+      case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true, true>, prm, kSolverThreads, kBiBlocksPerSM)
+                        : coop_launch(c, k_bicgstab3<5, NC, false, true>, prm, kSolverThreads, kBiBlocksPerSM);
+      case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true, true>, prm, kSolverThreads, kBiBlocksPerSM)
+                        : coop_launch(c, k_bicgstab3<7, NC, false, true>, prm, kSolverThreads, kBiBlocksPerSM);
+      default: return coop_launch(c, k_bicgstab3<0, NC, false, true>, prm, kSolverThreads, kBiBlocksPerSM);
     }
   }
   if ((c->k == 7 || c->k == 5) && !pov && c->nr <= kSingleBlockRowsPerThread * kSolverThreads &&
@@ -690,11 +688,11 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
     }
   }
   switch (c->k) {
-    case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm, kSolverThreads, FVB_BI_MINB)
-                      : coop_launch(c, k_bicgstab3<5, NC>, prm, kSolverThreads, FVB_BI_MINB);
-    case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm, kSolverThreads, FVB_BI_MINB)
-                      : coop_launch(c, k_bicgstab3<7, NC>, prm, kSolverThreads, FVB_BI_MINB);
-    default: return coop_launch(c, k_bicgstab3<0, NC>, prm, kSolverThreads, FVB_BI_MINB);
+    case 5: return sc ? coop_launch(c, k_bicgstab3<5, NC, true>, prm, kSolverThreads, kBiBlocksPerSM)
+                      : coop_launch(c, k_bicgstab3<5, NC>, prm, kSolverThreads, kBiBlocksPerSM);
+    case 7: return sc ? coop_launch(c, k_bicgstab3<7, NC, true>, prm, kSolverThreads, kBiBlocksPerSM)
+                      : coop_launch(c, k_bicgstab3<7, NC>, prm, kSolverThreads, kBiBlocksPerSM);
+    default: return coop_launch(c, k_bicgstab3<0, NC>, prm, kSolverThreads, kBiBlocksPerSM);
   }
 }
 
