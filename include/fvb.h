@@ -288,6 +288,16 @@ int fvb_state_apply_bcs(fvb_ctx* ctx, const double* u_speeds);
  * (coupling.py:206-213; the _plain_flux helper) */
 int fvb_op_face_flux(fvb_ctx* ctx, const double* values, const double* boundary,
                      double* flux_out);
+/* rhie_chow_flux (fvm.py:499-538): face fluxes S.u_f with the pressure-
+ * gradient smoothing D_f a_f [(p_N - p_O) - (grad p)_f . d] on internal
+ * faces and on boundary faces where p is value-pinned and u is not; 0 on
+ * u-empty faces.  u / ub SoA (3 x n_cells / 3 x n_boundary), p / pb, the
+ * momentum diagonal a_diag [n_cells] (FVB_E_FVM "zero momentum diagonal at
+ * cell N"), d SoA [3 x n_internal], d_boundary SoA [3 x n_boundary].  BC
+ * tables of the u (0) and p (1) fields must be set. */
+int fvb_op_rhie_chow(fvb_ctx* ctx, const double* u, const double* ub, const double* p,
+                     const double* pb, const double* a_diag, const double* d,
+                     const double* d_boundary, double* flux_out);
 /* plain flux S.u_f with 0 on empty faces (coupling.py:206-213) */
 int fvb_plain_flux(fvb_ctx* ctx);
 /* continuity_error (coupling.py:373-375) */
@@ -335,6 +345,7 @@ int fvb_set_sm_share(fvb_ctx* ctx, int share);
 #define FVB_SOLVER_EXPLICIT_INDEX 1 /* SpMV passes read int32 indices, not stencil codes */
 #define FVB_SOLVER_NO_RCM 2         /* solve in the mesh order on renumbered meshes */
 #define FVB_SOLVER_NO_CLUSTER 4     /* small systems on the plain grid / block path (no one-cluster or shared-memory solver) */
+#define FVB_STEP_NO_GRAPHS 8        /* launch the step's assembly kernels one by one instead of replaying their CUDA graphs */
 int fvb_set_solver_options(fvb_ctx* ctx, int flags);
 
 /* grid of the persistent solver kernels (no reference counterpart): at most

@@ -447,6 +447,34 @@ def gradient(f, g):
     return gr / g["cell_volume"].reshape((-1,) + (1,) * (gr.ndim - 1))
 
 
+def rhie_chow(u, p, a_diag, g):
+    """Rhie-Chow face fluxes (fvm.py:499-538): S.u_f, less D_f a_f
+    [(p_N - p_O) - (grad p)_f . d] on internal faces, the owner's D and d_b
+    on boundary faces where p is pinned and u is not, 0 on u-empty faces."""
+    m, ni = u.m, u.m["ni"]
+    if (a_diag == 0.0).any():
+        raise OracleError(f"zero momentum diagonal at cell {int(np.argmax(a_diag == 0.0))}")
+    own, nbr = m["own"], m["nbr"]
+    flux = _dot3(face_values(u, g), g["face_area"])
+    dc = g["cell_volume"] / a_diag
+    w = g["weight"]
+    df = w * dc[own[:ni]] + (1.0 - w) * dc[nbr]
+    a, _ = split_coeffs(g["face_area"][:ni], g["d"])
+    gp = gradient(p, g)
+    gpf = w[:, None] * gp[own[:ni]] + (1.0 - w[:, None]) * gp[nbr]
+    flux[:ni] -= df * a * ((p.values[nbr] - p.values[own[:ni]]) - _dot3(gpf, g["d"]))
+    uval, _, uem = u.masks()
+    pval, _, _ = p.masks()
+    sel = np.flatnonzero(pval & ~uval & ~uem)
+    if sel.size:
+        fb = ni + sel
+        ob = own[fb]
+        ab, _ = split_coeffs(g["face_area"][fb], g["d_boundary"][sel])
+        flux[fb] -= dc[ob] * ab * ((p.boundary[sel] - p.values[ob]) - _dot3(gp[ob], g["d_boundary"][sel]))
+    flux[ni:][uem] = 0.0
+    return flux
+
+
 def split_coeffs(S, d):
     """Over-relaxed split a = |S|^2/(S.d), k = S - a d (fvm.py:307-317)."""
     a = _dot3(S, S) / _dot3(S, d)

@@ -185,12 +185,13 @@ _sig("fvb_simple_sweep", I, vp, C.POINTER(StepCfgC), dp, C.POINTER(StepReportC))
 _sig("fvb_plain_flux", I, vp)
 _sig("fvb_state_apply_bcs", I, vp, dp)
 _sig("fvb_op_face_flux", I, vp, dp, dp, dp)
+_sig("fvb_op_rhie_chow", I, vp, dp, dp, dp, dp, dp, dp, dp, dp)
 _sig("fvb_continuity_error", I, vp, dp)
 _sig("fvb_sync", I, vp)
 _sig("fvb_set_solver_options", I, vp, C.c_int)
 _sig("fvb_set_solver_grid", I, vp, C.c_int)
 _sig("fvb_device_can_access_peer", I, C.c_int, C.c_int, C.POINTER(C.c_int))
-SOLVER_EXPLICIT_INDEX, SOLVER_NO_RCM, SOLVER_NO_CLUSTER = 1, 2, 4
+SOLVER_EXPLICIT_INDEX, SOLVER_NO_RCM, SOLVER_NO_CLUSTER, STEP_NO_GRAPHS = 1, 2, 4, 8
 _sig("fvb_pattern_codes", I, vp, C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int),
      C.POINTER(C.c_int64))
 _sig("fvb_launch_count", C.c_ulonglong)
@@ -211,7 +212,7 @@ EXPORTS = [
     "fvb_op_cg", "fvb_op_bicgstab", "fvb_op_bicgstab_batched", "fvb_op_apply_bcs",
     "fvb_op_interpolate", "fvb_op_gradient", "fvb_op_divergence", "fvb_op_laplacian",
     "fvb_op_laplacian_flux", "fvb_op_convection", "fvb_op_ddt", "fvb_piso_step",
-    "fvb_simple_sweep", "fvb_plain_flux", "fvb_state_apply_bcs", "fvb_op_face_flux", "fvb_continuity_error", "fvb_sync", "fvb_timer_start", "fvb_timer_stop",
+    "fvb_simple_sweep", "fvb_plain_flux", "fvb_state_apply_bcs", "fvb_op_face_flux", "fvb_op_rhie_chow", "fvb_continuity_error", "fvb_sync", "fvb_timer_start", "fvb_timer_stop",
     "fvb_launch_count", "fvb_pattern_codes", "fvb_set_solver_options", "fvb_set_solver_grid", "fvb_device_can_access_peer", "fvb_host_register", "fvb_host_unregister",
 ]
 

@@ -322,6 +322,17 @@ float ev_ms(Ctx* c, int a, int b) {
   return ms;
 }
 
+// Event record that becomes a timing node when the stream is being
+// captured into a step graph (a plain record otherwise).
+void rec(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &st);
+  if (st == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 // RunState.ops timing: an event pair around each operator of the step
 enum OpId { OP_DDT = 0, OP_CONV = 1, OP_LAP = 2, OP_GRAD = 3, OP_DIV = 4 };
 
@@ -329,11 +340,11 @@ int op_begin(Ctx* c, int op) {
   if (c->n_op >= Ctx::kOpEvents / 2) return -1;
   const int k = c->n_op++;
   c->op_id[k] = op;
-  cudaEventRecord(c->opev[2 * k], c->stream);
+  rec(c->opev[2 * k], c->stream);
   return k;
 }
 void op_end(Ctx* c, int k) {
-  if (k >= 0) cudaEventRecord(c->opev[2 * k + 1], c->stream);
+  if (k >= 0) rec(c->opev[2 * k + 1], c->stream);
 }
 void op_collect(Ctx* c, fvb_step_report* rep) {
   for (int k = 0; k < c->n_op; ++k) {
@@ -344,6 +355,74 @@ void op_collect(Ctx* c, fvb_step_report* rep) {
   }
   c->n_op = 0;
 }
+
+uint64_t fnv1a(const void* p, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+// One assembly segment of a step: the kernels, memsets and timing events
+// between two solver readbacks (host syncs).  The first time a segment
+// instance runs under a step configuration it is captured into a CUDA graph;
+// later steps replay the graph, one launch instead of 5-15 kernel launches,
+// memsets and event records (the small configs are launch-bound: C1 has 52
+// launches per step).  Kernel arguments are device pointers that never move
+// after the context's allocations and configuration scalars that are part
+// of the key, so a replay launches exactly the kernels a direct run would,
+// with the same arguments (same results, bitwise).  The host bookkeeping of
+// the segment (operator-timer ids, launch count) is recorded at capture and
+// re-applied on replay.  Decomposed contexts (their halo syncs talk to the
+// peers) and FVB_STEP_NO_GRAPHS run the body directly.
+template <class F>
+int step_segment(Ctx* c, const fvb_step_cfg* cfg, int id, int a, int b, F&& body) {
+  if (c->teamed() || (c->solver_flags & FVB_STEP_NO_GRAPHS)) return body();
+  if (c->seg_allocs != c->allocs.size()) {  // new allocations: pointers may have moved
+    for (auto& kv : c->segs) cudaGraphExecDestroy(kv.second.exec);
+    c->segs.clear();
+    c->seg_allocs = c->allocs.size();
+  }
+  // the key: segment instance, operator-timer position, options, and the
+  // step configuration without the time (no kernel reads cfg->t)
+  fvb_step_cfg kc = *cfg;
+  kc.t = 0.0;
+  const int key_ints[5] = {id, a, b, c->n_op, c->solver_flags};
+  const uint64_t key = fnv1a(&kc, sizeof kc, fnv1a(key_ints, sizeof key_ints));
+  auto it = c->segs.find(key);
+  if (it != c->segs.end()) {
+    const Ctx::Seg& sg = it->second;
+    for (int op : sg.ops) c->op_id[c->n_op++] = op;
+    g_launches.fetch_add(sg.launches, std::memory_order_relaxed);
+    FVB_CUDA(cudaGraphLaunch(sg.exec, c->stream));
+    return FVB_OK;
+  }
+  if (c->segs.size() >= 64) {  // the configuration keeps changing: start over
+    for (auto& kv : c->segs) cudaGraphExecDestroy(kv.second.exec);
+    c->segs.clear();
+  }
+  const int n_op0 = c->n_op;
+  const unsigned long long l0 = g_launches.load(std::memory_order_relaxed);
+  FVB_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const int rc = body();
+  cudaGraph_t g = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
+  if (rc != FVB_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  FVB_CUDA(ec);
+  Ctx::Seg sg;
+  const cudaError_t ei = cudaGraphInstantiate(&sg.exec, g, 0);
+  cudaGraphDestroy(g);
+  FVB_CUDA(ei);
+  sg.ops.assign(c->op_id + n_op0, c->op_id + c->n_op);
+  sg.launches = g_launches.load(std::memory_order_relaxed) - l0;
+  FVB_CUDA(cudaGraphLaunch(sg.exec, c->stream));
+  c->segs.emplace(key, std::move(sg));
+  return FVB_OK;
+}
+
+enum SegId { SEG_MOM_ASM = 1, SEG_MOM_RHS = 2, SEG_P_PRE = 3, SEG_P_ASM = 4, SEG_P_CORR = 5 };
 
 // _momentum_matrix (coupling.py:216-231)
 int momentum_matrix(Ctx* c, const fvb_step_cfg* cfg, bool with_ddt) {
@@ -384,31 +463,34 @@ int solve_momentum(Ctx* c, const fvb_step_cfg* cfg, bool relax, fvb_step_report*
   double* diag = c->slot(S_DIAG);
   double* gp = c->slot(S_GP);
   double* rhs = c->slot(S_RHS);
-  { k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, diag); fvb::note_launch(); }
-  const int tg = op_begin(c, OP_GRAD);
-  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
-  op_end(c, tg);
   const bool relaxing = relax && cfg->alpha_u < 1.0;
-  { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, nv, c->slot(S_B0), c->vol, gp, diag, c->u, rhs,
-                                           w.Vm, c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
-  FVB_CUDA(cudaGetLastError());
   // ||b_c|| of the three solve right-hand sides: block partials on the
   // device, read back with the solve's results (one host sync for both)
   const int sblocks = 2 * c->num_sms;
   double* spart = c->partials + kStepPartials;
-  { k_sumsq<<<sblocks, kThreads, 0, c->stream>>>(c->nr, nv, 3, rhs, spart); fvb::note_launch(); }
-  FVB_CUDA(cudaGetLastError());
+  FVB_TRY(step_segment(c, cfg, SEG_MOM_RHS, relaxing, 0, [&] {
+    { k_get_diag<<<g, kThreads, 0, c->stream>>>(n, c->diag_slot, w.Vm, diag); fvb::note_launch(); }
+    const int tg = op_begin(c, OP_GRAD);
+    FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+    op_end(c, tg);
+    { k_mom_rhs<<<g, kThreads, 0, c->stream>>>(n, nv, c->slot(S_B0), c->vol, gp, diag, c->u, rhs,
+                                             w.Vm, c->diag_slot, relaxing, cfg->alpha_u); fvb::note_launch(); }
+    FVB_CUDA(cudaGetLastError());
+    { k_sumsq<<<sblocks, kThreads, 0, c->stream>>>(c->nr, nv, 3, rhs, spart); fvb::note_launch(); }
+    FVB_CUDA(cudaGetLastError());
+    rec(c->ev[2], c->stream);
+    // the batched solve updates the three components in place; the reference
+    // solves them one by one and raises before assigning a failed one
+    // (coupling.py:259-277), so keep u to restore the unsolved components
+    FVB_CUDA(cudaMemcpyAsync(c->u_save, c->u, sizeof(double) * 3 * nv, cudaMemcpyDeviceToDevice,
+                             c->stream));
+    return FVB_OK;
+  }));
   std::vector<double> hpart(3 * size_t(sblocks));
   const Readback rb{spart, hpart.data(), 3 * sblocks};
-  FVB_CUDA(cudaEventRecord(c->ev[2], c->stream));
   const double* b[3] = {rhs, rhs + nv, rhs + 2 * nv};
   double* x[3] = {c->u, c->u + nv, c->u + 2 * nv};
   SolveOut out[3];
-  // the batched solve updates the three components in place; the reference
-  // solves them one by one and raises before assigning a failed one
-  // (coupling.py:259-277), so keep u to restore the unsolved components
-  FVB_CUDA(cudaMemcpyAsync(c->u_save, c->u, sizeof(double) * 3 * nv, cudaMemcpyDeviceToDevice,
-                           c->stream));
   FVB_TRY(bicgstab_solve(c, MatView{w.Vm, w.crsm}, 3, b, x, cfg->mom_tol, cfg->mom_abs_tol,
                          cfg->mom_max_iters, out, &rb));
   FVB_CUDA(cudaEventRecord(c->ev[3], c->stream));
@@ -462,42 +544,48 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
   double* rl = c->slot(S_RL);
   double* rp = c->slot(S_RP);
   double* pbefore = c->slot(S_PBEFORE);
-  FVB_CUDA(cudaEventRecord(c->ev[4], c->stream));
-  MatView Am{w.Vm, w.crsm};
-  for (int k = 0; k < 3; ++k) FVB_TRY(smvp(c, Am, c->u + k * nv, au + k * nv));
-  { k_hbya<<<g, kThreads, 0, c->stream>>>(n, nv, c->u, c->slot(S_B0), au, c->slot(S_DIAG), c->vol,
-                                        hv, rau); fvb::note_launch(); }
-  FVB_CUDA(cudaGetLastError());
-  FVB_TRY(team_halo(c, S_HV, 4));  // HbyA and rAU on processor faces
-  FVB_TRY(op_face_flux(c, 3, hv, c->ub, 0, w.phih));
-  const int td = op_begin(c, OP_DIV);
-  FVB_TRY(op_divergence(c, w.phih, divh));
-  op_end(c, td);
-  FVB_TRY(op_interp(c, -1, 1, rau, nullptr, w.rauf));
-  if (relax_p) FVB_CUDA(cudaMemcpyAsync(pbefore, c->p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c->stream));
-  FVB_CUDA(cudaEventRecord(c->ev[5], c->stream));
+  FVB_TRY(step_segment(c, cfg, SEG_P_PRE, relax_p, 0, [&] {
+    rec(c->ev[4], c->stream);
+    MatView Am{w.Vm, w.crsm};
+    for (int k = 0; k < 3; ++k) FVB_TRY(smvp(c, Am, c->u + k * nv, au + k * nv));
+    { k_hbya<<<g, kThreads, 0, c->stream>>>(n, nv, c->u, c->slot(S_B0), au, c->slot(S_DIAG), c->vol,
+                                          hv, rau); fvb::note_launch(); }
+    FVB_CUDA(cudaGetLastError());
+    FVB_TRY(team_halo(c, S_HV, 4));  // HbyA and rAU on processor faces
+    FVB_TRY(op_face_flux(c, 3, hv, c->ub, 0, w.phih));
+    const int td = op_begin(c, OP_DIV);
+    FVB_TRY(op_divergence(c, w.phih, divh));
+    op_end(c, td);
+    FVB_TRY(op_interp(c, -1, 1, rau, nullptr, w.rauf));
+    if (relax_p) FVB_CUDA(cudaMemcpyAsync(pbefore, c->p, sizeof(double) * nv, cudaMemcpyDeviceToDevice, c->stream));
+    rec(c->ev[5], c->stream);
+    return FVB_OK;
+  }));
   float asm_ms = 0.f, solve_ms = 0.f;
   const bool corr = cfg->nonorth_correction && cfg->limiter > 0.0;
   MatView Ap{w.Vp, w.crsp};
   for (int it = 0; it <= cfg->n_nonorth_correctors; ++it) {
-    FVB_CUDA(cudaEventRecord(c->ev[6], c->stream));
-    FVB_CUDA(cudaMemsetAsync(w.Vp, 0, sizeof(double) * c->k * size_t(n), c->stream));
-    if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsp, 0, sizeof(double) * c->nnz_crs, c->stream));
-    FVB_CUDA(cudaMemsetAsync(rl, 0, sizeof(double) * nv, c->stream));
-    const int tl = op_begin(c, OP_LAP);
-    if (corr) {
-      FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
-      FVB_TRY(team_halo(c, S_GP, 3));
-    }
-    FVB_TRY(op_laplacian(c, 1, 1, Ap, rl, 0.0, w.rauf, c->p, c->pb, gp,
-                         cfg->nonorth_correction, cfg->limiter, -1.0, w.coef, w.corr));
-    op_end(c, tl);
-    { k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, rl, divh, rp); fvb::note_launch(); }
-    if (cfg->pin_pressure)
-      { k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, rp, cfg->pressure_ref_cell,
-                                    cfg->pressure_ref_value); fvb::note_launch(); }
-    FVB_CUDA(cudaGetLastError());
-    FVB_CUDA(cudaEventRecord(c->ev[7], c->stream));
+    FVB_TRY(step_segment(c, cfg, SEG_P_ASM, it, 0, [&] {
+      rec(c->ev[6], c->stream);
+      FVB_CUDA(cudaMemsetAsync(w.Vp, 0, sizeof(double) * c->k * size_t(n), c->stream));
+      if (c->nnz_crs) FVB_CUDA(cudaMemsetAsync(w.crsp, 0, sizeof(double) * c->nnz_crs, c->stream));
+      FVB_CUDA(cudaMemsetAsync(rl, 0, sizeof(double) * nv, c->stream));
+      const int tl = op_begin(c, OP_LAP);
+      if (corr) {
+        FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+        FVB_TRY(team_halo(c, S_GP, 3));
+      }
+      FVB_TRY(op_laplacian(c, 1, 1, Ap, rl, 0.0, w.rauf, c->p, c->pb, gp,
+                           cfg->nonorth_correction, cfg->limiter, -1.0, w.coef, w.corr));
+      op_end(c, tl);
+      { k_p_rhs<<<g, kThreads, 0, c->stream>>>(n, rl, divh, rp); fvb::note_launch(); }
+      if (cfg->pin_pressure)
+        { k_pin<<<1, 1, 0, c->stream>>>(n, c->diag_slot, w.Vp, rp, cfg->pressure_ref_cell,
+                                      cfg->pressure_ref_value); fvb::note_launch(); }
+      FVB_CUDA(cudaGetLastError());
+      rec(c->ev[7], c->stream);
+      return FVB_OK;
+    }));
     SolveOut o;
     FVB_TRY(cg_solve(c, Ap, rp, c->p, cfg->p_tol, cfg->p_abs_tol, cfg->p_max_iters, &o));
     asm_ms += ev_ms(c, 6, 7);
@@ -519,26 +607,29 @@ int pressure_correct(Ctx* c, const fvb_step_cfg* cfg, bool relax_p, fvb_step_rep
   const bool defer = corr_index < Ctx::kTailPairs;
   cudaEvent_t e0 = defer ? c->cev[2 * corr_index] : c->ev[6];
   cudaEvent_t e1 = defer ? c->cev[2 * corr_index + 1] : c->ev[7];
-  FVB_CUDA(cudaEventRecord(e0, c->stream));
-  FVB_TRY(op_lap_flux(c, 1, 1, w.coef, w.corr, c->p, c->pb, w.lf));
-  { k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux); fvb::note_launch(); }
-  if (relax_p && cfg->alpha_p < 1.0) {
-    // the neighbours may still be reading the unrelaxed ghost p (their
-    // laplacian_face_flux): sync before overwriting it (write-after-read)
-    FVB_TRY(team_halo(c, S_P, 0));
-    { k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, pbefore, cfg->alpha_p); fvb::note_launch(); }
-    FVB_TRY(team_halo(c, S_P, 1));
-  }
-  FVB_CUDA(cudaGetLastError());
-  FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
-  const int tg = op_begin(c, OP_GRAD);
-  FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
-  op_end(c, tg);
-  { k_u_corr<<<g, kThreads, 0, c->stream>>>(n, nv, hv, rau, gp, c->u); fvb::note_launch(); }
-  FVB_CUDA(cudaGetLastError());
-  FVB_TRY(team_halo(c, S_U, 3));
-  FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
-  FVB_CUDA(cudaEventRecord(e1, c->stream));
+  FVB_TRY(step_segment(c, cfg, SEG_P_CORR, corr_index, relax_p, [&] {
+    rec(e0, c->stream);
+    FVB_TRY(op_lap_flux(c, 1, 1, w.coef, w.corr, c->p, c->pb, w.lf));
+    { k_flux_corr<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->nf, w.phih, w.lf, c->flux); fvb::note_launch(); }
+    if (relax_p && cfg->alpha_p < 1.0) {
+      // the neighbours may still be reading the unrelaxed ghost p (their
+      // laplacian_face_flux): sync before overwriting it (write-after-read)
+      FVB_TRY(team_halo(c, S_P, 0));
+      { k_relax_p<<<g, kThreads, 0, c->stream>>>(n, c->p, pbefore, cfg->alpha_p); fvb::note_launch(); }
+      FVB_TRY(team_halo(c, S_P, 1));
+    }
+    FVB_CUDA(cudaGetLastError());
+    FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
+    const int tg = op_begin(c, OP_GRAD);
+    FVB_TRY(op_gradient(c, 1, 1, c->p, c->pb, gp));
+    op_end(c, tg);
+    { k_u_corr<<<g, kThreads, 0, c->stream>>>(n, nv, hv, rau, gp, c->u); fvb::note_launch(); }
+    FVB_CUDA(cudaGetLastError());
+    FVB_TRY(team_halo(c, S_U, 3));
+    FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
+    rec(e1, c->stream);
+    return FVB_OK;
+  }));
   *t_asm += (ev_ms(c, 4, 5) + asm_ms) * 1e-3;  // complete: the CG readback synced
   *t_solve += solve_ms * 1e-3;
   if (defer) {
@@ -565,13 +656,16 @@ int run_step(Ctx* c, const fvb_step_cfg* cfg, const double* speeds, fvb_step_rep
   rep->p_res = -1.0;
   if (c->n_patches[0] && speeds)
     FVB_TRY(h2d(c, c->bc_speed[0], speeds, size_t(c->n_patches[0])));
-  FVB_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  if (piso) {  // piso_time_step applies BCs at the new time first (coupling.py:360-361)
-    FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
-    FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
-  }
-  FVB_TRY(momentum_matrix(c, cfg, piso));
-  FVB_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  FVB_TRY(step_segment(c, cfg, SEG_MOM_ASM, piso, 0, [&] {
+    rec(c->ev[0], c->stream);
+    if (piso) {  // piso_time_step applies BCs at the new time first (coupling.py:360-361)
+      FVB_TRY(op_apply_bcs(c, 0, 3, c->u, c->ub));
+      FVB_TRY(op_apply_bcs(c, 1, 1, c->p, c->pb));
+    }
+    FVB_TRY(momentum_matrix(c, cfg, piso));
+    rec(c->ev[1], c->stream);
+    return FVB_OK;
+  }));
   FVB_TRY(solve_momentum(c, cfg, !piso, rep));
   FVB_CUDA(cudaEventSynchronize(c->ev[3]));
   rep->t_momentum_assembly = ev_ms(c, 0, 1) * 1e-3;
@@ -660,6 +754,7 @@ int fvb_ctx_destroy(fvb_ctx* h) {
   Ctx* c = &h->c;
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->segs) cudaGraphExecDestroy(kv.second.exec);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
@@ -1388,6 +1483,36 @@ int fvb_op_face_flux(fvb_ctx* h, const double* values, const double* boundary,
   return sync(c);
 }
 
+int fvb_op_rhie_chow(fvb_ctx* h, const double* u, const double* ub, const double* p,
+                     const double* pb, const double* a_diag, const double* d, const double* d_boundary,
+                     double* flux_out) {
+  Ctx* c = &h->c;
+  cudaSetDevice(c->dev);
+  FVB_TRY(need_mesh(c));
+  FVB_TRY(need_bc(c, 0));
+  FVB_TRY(need_bc(c, 1));
+  for (int i = 0; i < c->nr; ++i)
+    if (a_diag[i] == 0.0) {
+      fvb_set_error("zero momentum diagonal at cell %d", i);
+      return FVB_E_FVM;
+    }
+  Tmp tu, tub, tp, tpb, ta, td, tdb, tg, tf;
+  double *du, *dub, *dp, *dpb, *da, *dd, *ddb, *dg, *df;
+  FVB_TRY(tmp_upload(c, tu, u, 3 * size_t(c->nc), &du));
+  FVB_TRY(tmp_upload(c, tub, ub, 3 * size_t(c->nb), &dub));
+  FVB_TRY(tmp_upload(c, tp, p, size_t(c->nc), &dp));
+  FVB_TRY(tmp_upload(c, tpb, pb, size_t(c->nb), &dpb));
+  FVB_TRY(tmp_upload(c, ta, a_diag, size_t(c->nc), &da));
+  FVB_TRY(tmp_upload(c, td, d, 3 * size_t(c->ni), &dd));
+  FVB_TRY(tmp_upload(c, tdb, d_boundary, 3 * size_t(c->nb), &ddb));
+  FVB_TRY(tmp_zero(c, tg, 3 * size_t(c->nc), &dg));
+  FVB_TRY(tmp_zero(c, tf, size_t(c->nf), &df));
+  FVB_TRY(op_gradient(c, 1, 1, dp, dpb, dg));
+  FVB_TRY(op_rhie_chow(c, du, dub, dp, dpb, da, dg, dd, ddb, df));
+  FVB_TRY(d2h(c, flux_out, df, size_t(c->nf)));
+  return sync(c);
+}
+
 int fvb_plain_flux(fvb_ctx* h) {
   Ctx* c = &h->c;
   cudaSetDevice(c->dev);
@@ -1589,7 +1714,8 @@ int fvb_simple_sweep(fvb_ctx* h, const fvb_step_cfg* cfg, const double* u_speeds
 }
 
 int fvb_set_solver_options(fvb_ctx* h, int flags) {
-  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM | FVB_SOLVER_NO_CLUSTER)) {
+  if (flags & ~(FVB_SOLVER_EXPLICIT_INDEX | FVB_SOLVER_NO_RCM | FVB_SOLVER_NO_CLUSTER |
+                FVB_STEP_NO_GRAPHS)) {
     fvb_set_error("unknown solver option bits 0x%x", flags);
     return FVB_E_ARG;
   }

@@ -16,6 +16,7 @@
 
 #include <atomic>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/fvb.h"
@@ -201,6 +202,16 @@ struct Ctx {
   cudaEvent_t opev[kOpEvents];
   int op_id[kOpEvents / 2];
   int n_op = 0;
+  // CUDA graphs of the step's assembly segments (step_segment, fvb_api.cu):
+  // captured on first use per segment instance and step configuration,
+  // replayed afterwards; dropped when the context allocates (new pointers)
+  struct Seg {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<int> ops;            // operator-timer ids the segment records
+    unsigned long long launches = 0; // kernel launches it holds
+  };
+  std::unordered_map<uint64_t, Seg> segs;
+  size_t seg_allocs = 0;             // allocs.size() the graphs were captured under
   int64_t bytes = 0;
   bool have_mesh = false, have_pattern = false;
   bool have_bc[2] = {false, false};
@@ -625,7 +636,9 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     if (gridDim.x == 1) {
       // small systems run on a single block: the block barrier is the grid
       // barrier (two barriers per reduction: the next reduction's first one
-      // orders the reuse of the broadcast slot)
+      // orders the reuse of the broadcast slot; a one-barrier variant in
+      // which every warp sums the warp partials itself measured slower,
+      // profiles/r02_small.md)
       block_reduce_lean<M>(v, smem);
       if (threadIdx.x == 0) {
 #pragma unroll
@@ -855,6 +868,9 @@ int op_ddt(Ctx* c, int ncomp, MatView A, double* rhs, const double* old, double 
            double coeff);
 int op_face_flux(Ctx* c, int ncomp_field, const double* vals, const double* bnd,
                  int field_for_mask, double* flux);
+int op_rhie_chow(Ctx* c, const double* u, const double* ub, const double* p, const double* pb,
+                 const double* adiag, const double* gp, const double* d, const double* db,
+                 double* flux);
 int op_precompute_geometry(Ctx* c, const double* dx, const double* dy,
                            const double* dz, const double* dbx, const double* dby,
                            const double* dbz);

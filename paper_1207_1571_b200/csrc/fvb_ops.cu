@@ -402,6 +402,46 @@ __global__ void k_face_flux(MeshView M, BcView B, const double* __restrict__ val
   }
 }
 
+// rhie_chow_flux (fvm.py:499-538): F = S . u_f, minus on internal faces
+// D_f a_f [(p_N - p_O) - (grad p)_f . d] with D = V / a_diag interpolated
+// linearly, and on boundary faces where p is pinned but u is not the same
+// with the owner's D and d_b; 0 on faces where u is empty.  Dot products in
+// the reference's einsum order (x + z) + y, as k_face_flux.
+__global__ void k_rhie_chow(MeshView M, BcView Bu, BcView Bp, const double* __restrict__ u,
+                            const double* __restrict__ ub, const double* __restrict__ p,
+                            const double* __restrict__ pb, const double* __restrict__ adiag,
+                            const double* __restrict__ gp, const double* __restrict__ d,
+                            const double* __restrict__ db, double* __restrict__ flux) {
+  const size_t nc = size_t(M.nc), ni = size_t(M.ni), nb = size_t(M.nb);
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < M.nf; f += gridDim.x * blockDim.x) {
+    const int j = f - M.ni;
+    if (f >= M.ni && Bu.kind[j] == FVB_BC_EMPTY) {
+      flux[f] = 0.0;
+      continue;
+    }
+    const double f0 = face_value(M, Bu, false, f, u, ub);
+    const double f1 = face_value(M, Bu, false, f, u + nc, ub + nb);
+    const double f2 = face_value(M, Bu, false, f, u + 2 * nc, ub + 2 * nb);
+    double F = (f0 * M.sx[f] + f2 * M.sz[f]) + f1 * M.sy[f];
+    const int o = M.own[f];
+    const double d_o = M.vol[o] / adiag[o];
+    if (f < M.ni) {
+      const int q = M.nbr[f];
+      const double w = M.w[f], w1 = 1.0 - w;
+      const double d_f = w * d_o + w1 * (M.vol[q] / adiag[q]);
+      const double g0 = w * gp[o] + w1 * gp[q];
+      const double g1 = w * gp[nc + o] + w1 * gp[nc + q];
+      const double g2 = w * gp[2 * nc + o] + w1 * gp[2 * nc + q];
+      const double gd = (g0 * d[f] + g2 * d[2 * ni + f]) + g1 * d[ni + f];
+      F -= (d_f * M.a[f]) * ((p[q] - p[o]) - gd);
+    } else if (bc_is_value(Bp.kind[j]) && !bc_is_value(Bu.kind[j])) {
+      const double gd = (gp[o] * db[j] + gp[2 * nc + o] * db[2 * nb + j]) + gp[nc + o] * db[nb + j];
+      F -= (d_o * M.a[f]) * ((pb[j] - p[o]) - gd);
+    }
+    flux[f] = F;
+  }
+}
+
 __global__ void k_inv_diag(int n, const int* __restrict__ ds, const double* __restrict__ V,
                            double* __restrict__ inv, int* first_zero) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -579,6 +619,15 @@ int op_face_flux(Ctx* c, int ncomp_field, const double* vals, const double* bnd,
   (void)ncomp_field;
   { k_face_flux<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(c->mesh(), c->bc(field_for_mask),
                                                                      vals, bnd, flux); fvb::note_launch(); }
+  FVB_CUDA(cudaGetLastError());
+  return FVB_OK;
+}
+
+int op_rhie_chow(Ctx* c, const double* u, const double* ub, const double* p, const double* pb,
+                 const double* adiag, const double* gp, const double* d, const double* db,
+                 double* flux) {
+  { k_rhie_chow<<<grid_for(c->nf, kThreads), kThreads, 0, c->stream>>>(
+        c->mesh(), c->bc(0), c->bc(1), u, ub, p, pb, adiag, gp, d, db, flux); fvb::note_launch(); }
   FVB_CUDA(cudaGetLastError());
   return FVB_OK;
 }

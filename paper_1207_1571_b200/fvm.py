@@ -27,7 +27,7 @@ __all__ = [
     "Field", "make_scalar", "make_vector", "apply_bcs", "interpolate_to_faces",
     "interpolate_cell_values", "face_divergence", "gauss_gradient", "LinearSystem",
     "LaplacianFaceData", "laplacian", "laplacian_face_flux", "divergence_convection",
-    "ddt_euler", "TWO_PI",
+    "ddt_euler", "rhie_chow_flux", "TWO_PI",
 ]
 
 
@@ -315,6 +315,17 @@ def laplacian(sys, gamma, field, geom, scheme, coeff=1.0):
     """Add coeff*laplacian(gamma, phi) to the system (fvm.py:335-408); returns face data."""
     mesh = field.mesh
     gs, gf = _face_gamma(gamma, mesh.n_faces)
+    if geom is not None:
+        # the reference validates the geometry object it is handed
+        # (fvm.py:353-354, 369-371), which may differ from the context's
+        # device copy (a caller can edit it): same checks, same messages
+        zero = np.flatnonzero(np.asarray(geom.d_mag) == 0.0)
+        if zero.size:
+            raise FvmError(f"coincident centroids at internal face {int(zero[0])}")
+        value_m, _, _ = _boundary_masks(field)
+        bad = np.flatnonzero(value_m & (np.asarray(geom.d_boundary_mag) == 0.0))
+        if bad.size:
+            raise FvmError(f"coincident centroids at boundary face {int(bad[0]) + mesh.n_internal}")
     ctx, geom = _mesh_ctx(mesh, geom, sys.pattern)
     slot, _ = set_field_bcs(ctx, field, geom)
     nc = _ncomp(field)
@@ -384,3 +395,23 @@ def ddt_euler(sys, field, old_values, dt, geom, coeff=1.0):
                FvmError)
     sys.A.V[...] = V
     sys.rhs[...] = _aos(rhs, nc, sys.pattern.n)
+
+
+def rhie_chow_flux(u, p_field, a_diag, geom):
+    """Face volume fluxes with Rhie-Chow pressure smoothing (fvm.py:499-538):
+    S . u_f, less D_f a_f [(p_N - p_O) - (grad p)_f . d] on internal faces
+    (D = V / a_diag interpolated to the face) and on boundary faces where p
+    is pinned and u is not; 0 where u is empty.  One gradient and one face
+    kernel on the device (fvb_op_rhie_chow)."""
+    mesh = u.mesh
+    ctx, geom = _mesh_ctx(mesh, geom)
+    set_field_bcs(ctx, u, geom)
+    set_field_bcs(ctx, p_field, geom)
+    a = _lib.f64(a_diag)
+    out = np.empty(mesh.n_faces)
+    P = _lib.ptr
+    _lib.check(_lib.lib.fvb_op_rhie_chow(
+        ctx.h, P(_soa(u.values, 3)), P(_soa(u.boundary, 3)), P(_lib.f64(p_field.values)),
+        P(_lib.f64(p_field.boundary)), P(a), P(_soa(geom.d, 3)), P(_soa(geom.d_boundary, 3)),
+        P(out)), FvmError)
+    return out

@@ -21,7 +21,7 @@ RESIDUAL_FLOOR = 1e-30
 BREAKDOWN_EPS = 1e-300
 
 __all__ = ["STAGES", "SolverError", "SolveConfig", "SolveReport", "cg", "bicgstab",
-           "bicgstab_batched", "residual_norm"]
+           "bicgstab_batched", "residual_norm", "jacobi_apply"]
 
 
 @dataclass
@@ -109,6 +109,17 @@ def bicgstab_batched(A, B, X0, cfg: SolveConfig):
     x, reps = _solve(_lib.lib.fvb_op_bicgstab_batched, A, Bs.reshape(-1), Xs.reshape(-1), cfg,
                      ncomp=Bs.shape[0])
     return x.reshape(Bs.shape).T.copy(), reps
+
+
+def jacobi_apply(diag, r):
+    """z = r / diag, the Jacobi preconditioner as a standalone helper
+    (linsolve.py:82-87; the device solvers fuse it into their passes).
+    SolverError names the first zero diagonal row, as the solvers do."""
+    diag = np.asarray(diag, dtype=float)
+    bad = np.flatnonzero(diag == 0.0)
+    if bad.size:
+        raise SolverError(f"singular preconditioner: zero diagonal at row {int(bad[0])}")
+    return np.asarray(r, dtype=float) / diag
 
 
 def residual_norm(A, x, b):

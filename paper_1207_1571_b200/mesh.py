@@ -141,6 +141,22 @@ class MeshGeometry:
         return float(self.nonorth_deg.max()) if len(self.nonorth_deg) else 0.0
 
 
+def _face_triangles(mesh):
+    """The fan triangles fvb_geometry integrates over (reference helper
+    mesh.py:154-170): for every loop edge (p_k, p_k+1) of a face, the
+    triangle (p_k, p_k+1, seed) with seed the mean of the face's points.
+    Returns (a, b, seed per triangle, face per triangle)."""
+    off = np.asarray(mesh.face_offsets, dtype=np.int64)
+    fp = np.asarray(mesh.face_points, dtype=np.int64)
+    npts = off[1:] - off[:-1]
+    tri_face = np.repeat(np.arange(len(npts)), npts)
+    k = np.arange(len(fp)) - off[tri_face]        # position of the edge in its loop
+    succ = off[tri_face] + (k + 1) % npts[tri_face]
+    pts = np.asarray(mesh.points, dtype=float)
+    seeds = np.add.reduceat(pts[fp], off[:-1], axis=0) / npts[:, None]
+    return pts[fp], pts[fp[succ]], seeds[tri_face], tri_face
+
+
 def compute_geometry(mesh, check=True) -> MeshGeometry:
     """Native fan-triangle / tet-decomposition metrics (fvb_geometry).
 

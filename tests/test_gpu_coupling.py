@@ -164,3 +164,53 @@ def test_one_step_reseeded_from_oracle_state(maker, algo):
         if a[1] == "uz" and case.mesh.n_cells in (1040,):
             continue  # one-cell-thick mesh: round-off-driven uz solve
         assert abs(a[3] - b[3]) <= (1 if a[0] == "cg" else 2), (a, b)
+
+
+def _cavity_2d():
+    """C1 (BASELINE configs[0]): 2D lid-driven cavity 20x20x1, PISO dt 0.005."""
+    from paper_1207_1571_b200.cases import Case
+    from paper_1207_1571_b200.config import BoundarySpec, CaseConfig
+
+    m = cases.box_mesh(20, 20, 1, 0.1, 0.1, 0.01,
+                       [("movingWall", "wall", ["y+"]), ("fixedWalls", "wall", ["x-", "x+", "y-"]),
+                        ("frontAndBack", "empty", ["z-", "z+"])])
+    cc = CaseConfig()
+    cc.nu, cc.algorithm, cc.dt, cc.end_time = 0.01, "piso", 0.005, 0.5
+    cc.boundary = {"movingWall": BoundarySpec(u=("fixed_value", (1.0, 0.0, 0.0)), p=("zero_gradient",)),
+                   "fixedWalls": BoundarySpec(u=("no_slip",), p=("zero_gradient",)),
+                   "frontAndBack": BoundarySpec(u=("empty",), p=("empty",))}
+    return Case("c1", m, cc)
+
+
+def _bfs_simple():
+    case = cases.gen_backward_step(4)
+    case.config.algorithm = "simple"
+    return case
+
+
+@pytest.mark.parametrize("maker", [_cavity_2d, _bfs_simple, lambda: cases.gen_cavity(10)])
+def test_step_graph_replay_is_bitwise(maker):
+    """The step's assembly segments run as captured CUDA graphs (fvb_api.cu
+    step_segment) from the second step on: fields, residual logs, operator
+    call counts and the number of kernels launched must be exactly those of
+    launching every kernel directly (FVB_STEP_NO_GRAPHS)."""
+    from paper_1207_1571_b200 import _lib
+
+    def run(flags):
+        case = maker()
+        cfg = CouplingConfig.from_case_config(case.config)
+        st = init_state(case, cfg)
+        _lib.check(_lib.lib.fvb_set_solver_options(st._ctx.h, flags))
+        l0 = _lib.lib.fvb_launch_count()
+        for _ in range(5):
+            step(st, cfg)
+        return st, _lib.lib.fvb_launch_count() - l0
+
+    a, la = run(0)
+    b, lb = run(_lib.STEP_NO_GRAPHS)
+    assert np.array_equal(a.u.values, b.u.values) and np.array_equal(a.p.values, b.p.values)
+    assert np.array_equal(a.flux, b.flux)
+    assert a.residual_log == b.residual_log
+    assert {k: v[1] for k, v in a.ops.items()} == {k: v[1] for k, v in b.ops.items()}
+    assert la == lb > 0
+    assert all(a.wall[k] > 0.0 for k in ("momentum_assembly", "pressure_assembly", "correction"))

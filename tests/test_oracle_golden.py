@@ -2,10 +2,12 @@
 REAL reference produced (oracle/make_golden.py).  This pins the oracle
 before any CUDA result is compared with it."""
 
+import os
+
 import numpy as np
 import pytest
 
-from golden_io import CASES, golden_case, rel
+from golden_io import CASES, GOLDEN, golden_case, rel
 from oracle import fvoracle as O
 
 
@@ -85,3 +87,26 @@ def test_oracle_coupled_steps(name):
         log = g[f"s{s}_log"]
         mine = np.array([r[3] for r in run.log[-len(log):]])
         assert np.abs(mine - log[:, 1]).max() <= 1
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_rhie_chow_vs_reference(name):
+    """oracle.rhie_chow against the real reference's rhie_chow_flux
+    (fvm.py:499-538; tests/golden/rhie.npz, oracle/make_golden_rhie.py)."""
+    case, g = golden_case(name)
+    with np.load(os.path.join(GOLDEN, "rhie.npz")) as z:
+        a_diag, want = z[f"{name}_a_diag"], z[f"{name}_flux"]
+    m = O.mesh_arrays(case.mesh)
+    geo = O.geometry(m)
+    ub = {n: O.bc_kind(s.u) for n, s in case.config.boundary.items()}
+    pb = {n: O.bc_kind(s.p) for n, s in case.config.boundary.items()}
+    u = O.BField(m, ub, g["in_u"].copy())
+    p = O.BField(m, pb, g["in_p"].copy())
+    O.apply_bcs(u, geo, float(g["in_t"]))
+    O.apply_bcs(p, geo, float(g["in_t"]))
+    got = O.rhie_chow(u, p, a_diag, geo)
+    assert np.array_equal(got, want), rel(got, want)
+    bad = a_diag.copy()
+    bad[3] = 0.0
+    with pytest.raises(O.OracleError, match="cell 3"):
+        O.rhie_chow(u, p, bad, geo)

@@ -1,0 +1,69 @@
+"""Drop-in conformance: the reference's own unit tests (fvflow
+pkg/tests/test_{mesh,sparse,linsolve,fvm,coupling}.py) run UNMODIFIED
+against this package, with `fvflow.<module>` aliased to
+`paper_1207_1571_b200.<module>` (tools/fvflow_alias.py; VERDICT r01
+"missing" item 6).
+
+    python tools/ref_conformance.py stage      # copy the test files (needs /root/reference)
+    python tools/ref_conformance.py run [-k ...] # pytest them, JSON summary on stdout
+
+The reference tests are not part of this repository: `stage` copies them
+into baseline/_ref_tests/ (git-ignored like baseline/_ref, but not
+gpurun-ignored, so a staged copy travels to the GPU box).  Every numerical
+call of the run goes through libfvb on the device; tests that need no
+device (mesh validation, pattern building) run on the native CPU builder.
+"""
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+SRC = "/root/reference/pkg/tests"
+DST = os.path.join(ROOT, "baseline", "_ref_tests")
+FILES = ("conftest.py", "helpers_mms.py", "test_mesh.py", "test_sparse.py", "test_linsolve.py",
+         "test_fvm.py", "test_coupling.py")
+
+
+def stage():
+    os.makedirs(DST, exist_ok=True)
+    for f in FILES:
+        shutil.copy(os.path.join(SRC, f), os.path.join(DST, f))
+    print(DST)
+
+
+def run(extra):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([HERE, ROOT, env.get("PYTHONPATH", "")])
+    junit = os.path.join(ROOT, "gpurun_out", "ref_conformance.xml")
+    os.makedirs(os.path.dirname(junit), exist_ok=True)
+    tests = [os.path.join(DST, f) for f in FILES if f.startswith("test_")]
+    cmd = [sys.executable, "-m", "pytest", "-p", "fvflow_alias", "-q", "-rf", "--tb=line",
+           "-p", "no:cacheprovider", f"--junitxml={junit}", "--rootdir", DST, *tests, *extra]
+    r = subprocess.run(cmd, cwd=DST, env=env, capture_output=True, text=True)
+    sys.stderr.write(r.stdout[-6000:] + r.stderr[-2000:])
+    import xml.etree.ElementTree as ET
+    out = {"files": {}, "failed": []}
+    for case in ET.parse(junit).getroot().iter("testcase"):
+        f = case.get("classname", "").split(".")[0]
+        d = out["files"].setdefault(f, {"passed": 0, "failed": 0, "skipped": 0})
+        if case.find("failure") is not None or case.find("error") is not None:
+            d["failed"] += 1
+            node = case.find("failure") if case.find("failure") is not None else case.find("error")
+            out["failed"].append({"test": f"{f}::{case.get('name')}",
+                                  "message": (node.get("message") or "")[:300]})
+        elif case.find("skipped") is not None:
+            d["skipped"] += 1
+        else:
+            d["passed"] += 1
+    print(json.dumps(out, indent=1))
+    return r.returncode
+
+
+if __name__ == "__main__":
+    if sys.argv[1:2] == ["stage"]:
+        stage()
+    else:
+        sys.exit(run(sys.argv[2:]))
