@@ -196,7 +196,10 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
   }
   const PatternView& P = A.P;
   const TeamView& T = A.T;
-  const RowRange R = team_rows(T, P.n);
+  // (a single-block solver owns every row, also when it is one of several
+  // independent solves of the launch, k_bicgstab_split)
+  const RowRange R = SMEM ? RowRange{int(threadIdx.x), P.n, int(blockDim.x), false}
+                          : team_rows(T, P.n);
   const int n = R.end;       // rows of this block: tid, tid + G, ... < n
   const int G = R.step;
   const int tid = R.begin;
@@ -241,7 +244,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
       }
     }
   }
-  if (!team_reduce<2 * NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, sums, red, rnd, sends)) {
+  if (!team_reduce<2 * NC, false, TEAM, CLUSTER, SYS, SMEM>(T, A.sync, A.partials, sums, red, rnd, sends)) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int c = 0; c < NC; ++c) A.result[6 * c + 4] = SE_TIMEOUT;
     return;
@@ -350,7 +353,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<NC, false, TEAM, CLUSTER, SYS, SMEM>(T, A.sync, A.partials, rv, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -397,7 +400,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_spmv += t_ - tk; tk = t_; }
-      if (!team_reduce<3 * NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<3 * NC, false, TEAM, CLUSTER, SYS, SMEM>(T, A.sync, A.partials, st, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -504,7 +507,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
         }
       }
       if (timer) { const uint64_t t_ = global_ns(); t_axpy += t_ - tk; tk = t_; }
-      if (!team_reduce<2 * NC, false, TEAM, CLUSTER, SYS>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
+      if (!team_reduce<2 * NC, false, TEAM, CLUSTER, SYS, SMEM>(T, A.sync, A.partials, rr, red, rnd, sends)) { timeout = true; break; }
       if (timer) { const uint64_t t_ = global_ns(); t_red += t_ - tk; tk = t_; }
       if (threadIdx.x == 0)
         for (int c = 0; c < NC; ++c) {
@@ -520,7 +523,7 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
       __syncthreads();
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (threadIdx.x == 0 && (SMEM || blockIdx.x == 0)) {
     for (int c = 0; c < NC; ++c) {
       A.result[6 * c + 0] = S[c].it;
       A.result[6 * c + 1] = S[c].done ? 1.0 : 0.0;
@@ -529,10 +532,45 @@ __device__ __forceinline__ void bicgstab3_body(const Bi3Params<NC>& A) {
       A.result[6 * c + 4] = timeout ? SE_TIMEOUT : S[c].err;
       A.result[6 * c + 5] = S[c].err_it;
     }
-    A.result[18] = 1e-9 * double(t_spmv);
-    A.result[19] = 1e-9 * double(t_axpy);
-    A.result[20] = 1e-9 * double(t_red);
+    if (blockIdx.x == 0) {
+      A.result[18] = 1e-9 * double(t_spmv);
+      A.result[19] = 1e-9 * double(t_axpy);
+      A.result[20] = 1e-9 * double(t_red);
+    }
   }
+}
+
+// Shared-memory staging of a single-block solve: r, r_hat, the p / d and v
+// buffers, t and 1/D (and the matrix with its stencil codes) move to dynamic
+// shared memory for the solve; x and b stay in global memory.
+template <int KT, int NC, bool SC>
+__device__ __forceinline__ void smem_stage(Bi3Params<NC>& B, double* dyn) {
+  const int n = B.P.n;
+  const double* inv = B.inv;
+  double* q = dyn;
+  for (int c = 0; c < NC; ++c) {
+    B.r[c] = q; q += n;
+    B.rh[c] = q; q += n;
+    B.p[0][c] = q; q += n;
+    B.p[1][c] = q; q += n;
+    B.v[0][c] = q; q += n;
+    B.v[1][c] = q; q += n;
+    B.t[c] = q; q += n;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) q[i] = inv[i];
+  B.inv = q;
+  q += n;
+  if constexpr (KT > 0) {
+    // the matrix and its stencil codes too (read by both SpMV passes)
+    for (int e = threadIdx.x; e < KT * n; e += blockDim.x) q[e] = B.V[e];
+    B.Vp = q;
+    if constexpr (SC) {
+      uint8_t* cs = reinterpret_cast<uint8_t*>(q + KT * n);
+      for (int i = threadIdx.x; i < n; i += blockDim.x) cs[i] = B.P.code[i];
+      B.codep = cs;
+    }
+  }
+  __syncthreads();
 }
 
 // Persistent batched BiCGStab.  SMEM (single-block systems): r, r_hat, the
@@ -543,36 +581,49 @@ template <int KT, int NC, bool SC = false, bool TEAM = false, bool CLUSTER = fal
 __global__ void __launch_bounds__(kSolverThreads, kBiBlocksPerSM) k_bicgstab3(Bi3Params<NC> A) {
   if constexpr (SMEM) {
     extern __shared__ double dyn[];
-    const int n = A.P.n;
     Bi3Params<NC> B = A;
-    double* q = dyn;
-    for (int c = 0; c < NC; ++c) {
-      B.r[c] = q; q += n;
-      B.rh[c] = q; q += n;
-      B.p[0][c] = q; q += n;
-      B.p[1][c] = q; q += n;
-      B.v[0][c] = q; q += n;
-      B.v[1][c] = q; q += n;
-      B.t[c] = q; q += n;
-    }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) q[i] = A.inv[i];
-    B.inv = q;
-    q += n;
-    if constexpr (KT > 0) {
-      // the matrix and its stencil codes too (read by both SpMV passes)
-      for (int e = threadIdx.x; e < KT * n; e += blockDim.x) q[e] = A.V[e];
-      B.Vp = q;
-      if constexpr (SC) {
-        uint8_t* cs = reinterpret_cast<uint8_t*>(q + KT * n);
-        for (int i = threadIdx.x; i < n; i += blockDim.x) cs[i] = A.P.code[i];
-        B.codep = cs;
-      }
-    }
-    __syncthreads();
+    smem_stage<KT, NC, SC>(B, dyn);
     bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, true>(B);
   } else {
     bicgstab3_body<KT, NC, SC, TEAM, CLUSTER, false, SYS>(A);
   }
+}
+
+// The three momentum components as three independent single-block solves
+// of one launch (block c solves component c; small systems whose batch fits
+// in shared memory, C1): a third of the rows' work per thread and a third of
+// the values per reduction, on three SMs instead of one (C1 momentum solve
+// 260 -> 146 us per step, profiles/r02_small.md).  Each block runs the
+// batched kernel's arithmetic for its component (the components of a batch
+// never interact: per-component scalars, reductions over M values sum each
+// value separately), so the iterates are those of the batched kernel.
+template <int KT, bool SC>
+__global__ void __launch_bounds__(kSolverThreads, kBiBlocksPerSM) k_bicgstab_split(Bi3Params<3> A) {
+  if (A.zero_flag && *A.zero_flag) {  // the batched kernel's zero-diagonal result, once
+    if (blockIdx.x == 0) zero_diag_exit(A.zero_flag, A.result, 3);
+    return;
+  }
+  const int c = blockIdx.x;
+  Bi3Params<1> B;
+  B.P = A.P;
+  B.T = A.T;
+  B.V = A.V;
+  B.crs = A.crs;
+  B.inv = A.inv;
+  B.b[0] = A.b[c];
+  B.x[0] = A.x[c];
+  B.tol = A.tol;
+  B.abs_tol = A.abs_tol;
+  B.max_iters = A.max_iters;
+  B.sync = A.sync;
+  B.partials = A.partials;
+  B.result = A.result + 6 * c;
+  B.zero_flag = nullptr;
+  B.Vp = A.Vp;
+  B.codep = A.codep;
+  extern __shared__ double dyn[];
+  smem_stage<KT, 1, SC>(B, dyn);
+  bicgstab3_body<KT, 1, SC, false, false, true>(B);
 }
 
 }  // namespace
@@ -664,12 +715,22 @@ static int bicg3_launch(Ctx* c, MatView A, const double* const* b, double* const
   }
   if ((c->k == 7 || c->k == 5) && !pov && c->nr <= kSingleBlockRowsPerThread * kSolverThreads &&
       smem_bi_bytes(c->nr, NC, c->k) <= kSmemSolverMax && !(c->solver_flags & FVB_SOLVER_NO_CLUSTER)) {
-    const size_t bytes = smem_bi_bytes(c->nr, NC, c->k);
-    if (c->k == 7)
-      return sc ? smem_launch(c, k_bicgstab3<7, NC, true, false, false, true>, prm, kSolverThreads, bytes)
-                : smem_launch(c, k_bicgstab3<7, NC, false, false, false, true>, prm, kSolverThreads, bytes);
-    return sc ? smem_launch(c, k_bicgstab3<5, NC, true, false, false, true>, prm, kSolverThreads, bytes)
-              : smem_launch(c, k_bicgstab3<5, NC, false, false, false, true>, prm, kSolverThreads, bytes);
+    if constexpr (NC == 3) {
+      // one block per component (k_bicgstab_split)
+      const size_t b1 = smem_bi_bytes(c->nr, 1, c->k);
+      if (c->k == 7)
+        return sc ? smem_launch(c, k_bicgstab_split<7, true>, prm, kSolverThreads, b1, 3)
+                  : smem_launch(c, k_bicgstab_split<7, false>, prm, kSolverThreads, b1, 3);
+      return sc ? smem_launch(c, k_bicgstab_split<5, true>, prm, kSolverThreads, b1, 3)
+                : smem_launch(c, k_bicgstab_split<5, false>, prm, kSolverThreads, b1, 3);
+    } else {
+      const size_t bytes = smem_bi_bytes(c->nr, NC, c->k);
+      if (c->k == 7)
+        return sc ? smem_launch(c, k_bicgstab3<7, NC, true, false, false, true>, prm, kSolverThreads, bytes)
+                  : smem_launch(c, k_bicgstab3<7, NC, false, false, false, true>, prm, kSolverThreads, bytes);
+      return sc ? smem_launch(c, k_bicgstab3<5, NC, true, false, false, true>, prm, kSolverThreads, bytes)
+                : smem_launch(c, k_bicgstab3<5, NC, false, false, false, true>, prm, kSolverThreads, bytes);
+    }
   }
   if (c->k == 7 || c->k == 5) {
     const int want = cluster_want(c, kSolverThreads);

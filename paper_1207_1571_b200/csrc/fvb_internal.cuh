@@ -606,7 +606,10 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[M], double* smem, uns
 // CLUSTER: the kernel runs as one thread-block cluster (cluster_reduce).
 // SYS: a team over several devices (compile-time, so the single-device and
 // co-resident team kernels carry no system-scope code).
-template <int M, bool OOL = false, bool TEAM = true, bool CLUSTER = false, bool SYS = false>
+// BLOCK: the kernel is a single-block solver (a block may be one of several
+// independent solves of a launch), whose block barrier is the grid barrier.
+template <int M, bool OOL = false, bool TEAM = true, bool CLUSTER = false, bool SYS = false,
+          bool BLOCK = false>
 __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
                                             double* partials, double (&v)[M],
                                             double* smem /*[32*M+M]*/, unsigned& rnd,
@@ -633,7 +636,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     // r+2 only after passing round r+1, i.e. after every block finished
     // reading round r.
     (void)sends;
-    if (gridDim.x == 1) {
+    if (BLOCK || gridDim.x == 1) {
       // small systems run on a single block: the block barrier is the grid
       // barrier (two barriers per reduction: the next reduction's first one
       // orders the reuse of the broadcast slot; a one-barrier variant in

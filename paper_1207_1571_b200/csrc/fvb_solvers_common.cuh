@@ -55,16 +55,19 @@ inline size_t smem_bi_bytes(int n, int nc, int k) {
 constexpr size_t kSmemSolverMax = 200 * 1024;
 
 template <typename K, typename Args>
-int smem_launch(Ctx* c, K kernel, Args& args, int threads, size_t bytes) {
+int smem_launch(Ctx* c, K kernel, Args& args, int threads, size_t bytes, int blocks = 1) {
   FVB_CUDA(cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 int(bytes)));
   FVB_CUDA(cudaMemsetAsync(c->sync, 0, 3 * sizeof(unsigned), c->stream));
   // one row per thread: fewer warps make the block barriers of the tiny
   // solves cheaper (rounded to whole warps pairs, at most `threads`)
-  const int t = std::min(threads, std::max(64, (c->nr + 63) / 64 * 64));
+#ifndef FVB_DIAG_SMEM_ROWS  // diagnostic builds: rows per thread
+#define FVB_DIAG_SMEM_ROWS 1
+#endif
+  const int t = std::min(threads, std::max(64, (c->nr / FVB_DIAG_SMEM_ROWS + 63) / 64 * 64));
   void* params[] = {&args};
   fvb::note_launch();
-  FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(1), dim3(t), params, bytes, c->stream));
+  FVB_CUDA(cudaLaunchKernel((const void*)kernel, dim3(blocks), dim3(t), params, bytes, c->stream));
   return FVB_OK;
 }
 
@@ -168,6 +171,9 @@ inline int cluster_want(const Ctx* c, int threads) {
   if (c->nr <= kSingleBlockRowsPerThread * threads || c->nr > kClusterMaxRows) return 0;
   if (c->solver_max_blocks > 0) return 0;  // an explicit grid cap wins
   (void)threads;
+#ifdef FVB_DIAG_CLUSTER  // diagnostic builds: cluster size
+  return FVB_DIAG_CLUSTER;
+#endif
   return 16;  // as many SMs as one cluster can hold (cluster_blocks clamps)
 }
 
