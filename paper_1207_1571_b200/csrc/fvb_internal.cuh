@@ -79,9 +79,26 @@ struct Comm {
   unsigned long long epoch;                      // local: team syncs completed
   unsigned long long pad[7];
   double mail[2][kMaxTeam][kMailM];              // [epoch parity][sender][payload]
+  // solver reductions of a decomposed mesh (team_reduce): arrivals of every
+  // rank's blocks (written by the peers), rounds this rank completed
+  unsigned long long tr_arrive;
+  unsigned long long tr_round;  // reductions this rank completed (all launches)
+  unsigned long long tr_base;   // block arrivals those reductions took (grids differ per kernel)
 };
-constexpr size_t kCommBytes = 4096;
-static_assert(sizeof(Comm) <= kCommBytes, "comm area");
+// team-partials buffer of the solver reductions, after the comm struct:
+// [round parity][sender rank][value][sender block], written by the peers
+constexpr unsigned long long kReduceTimeoutMark = 0xFEEDFACE00000000ull;  // Comm::pad[6]
+constexpr int kTeamGridMax = 512;  // blocks of a team solver grid (coop_blocks caps)
+constexpr size_t kTeamPartOffset = 4096;
+constexpr size_t kTeamPartBytes = size_t(2) * kMaxTeam * 16 * kTeamGridMax * sizeof(double);
+constexpr size_t kCommBytes = kTeamPartOffset + kTeamPartBytes;
+static_assert(sizeof(Comm) <= kTeamPartOffset, "comm area");
+__host__ __device__ inline double* team_part(Comm* c) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(c) + kTeamPartOffset);
+}
+__host__ __device__ inline size_t team_part_index(int par, int rank, int m, int block) {
+  return ((size_t(par) * kMaxTeam + size_t(rank)) * 16 + size_t(m)) * kTeamGridMax + size_t(block);
+}
 
 // Device view of the team: who the peers are and where their pools are.
 struct TeamView {
@@ -601,6 +618,13 @@ __device__ __forceinline__ void cluster_reduce(double (&v)[M], double* smem, uns
   // reuse of smem and s_all)
 }
 
+// Per-block copies of the rank's round and arrival counts at the launch's
+// first team reduction.  Namespace scope, not inside team_reduce: each
+// instantiation (M = 1, 2, 3, ...) of a function-scope __shared__ variable
+// would be a different variable.
+static __shared__ unsigned long long s_team_round0;
+static __shared__ unsigned long long s_team_arrive0;
+
 // TEAM = false: the kernel instantiation for a single domain, which
 // compiles the team path away (it costs registers in the solver loops).
 // CLUSTER: the kernel runs as one thread-block cluster (cluster_reduce).
@@ -619,8 +643,7 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     return true;
   }
   static_assert(M <= int(kRedStride), "team_reduce: at most kRedStride values");
-  __shared__ int s_last, s_ok;
-  __shared__ unsigned s_gen;
+  __shared__ int s_ok;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #ifdef FVB_DIAG_FENCE  // diagnostic build (tools/build_variant.py): every thread fences
   __threadfence();
@@ -701,100 +724,120 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
 #endif
     return ok;
   }
-  // teamed: the result goes through the peer mailboxes (broadcast path);
-  // sys: the peers are other devices, so arrivals order this block's halo
-  // stores at system scope
-  const bool teamed = T.size > 1;
-  // Multi-device team (SYS kernels): every block's arrival is a system-scope
-  // acq_rel atomic, so its halo stores to the peers (NVLink) are ordered
-  // before the last arriver's mailbox flags by the storing block itself —
-  // not only through the cumulativity of the last arriver's fence.sc.sys,
-  // which a gpu-scope arrival would rely on.  One device (all
-  // ranks co-resident, tests): gpu scope.  (A gpu-scope arrival measured
-  // ~6 us less per reduction on one device, profiles/r01_team.md, but a
-  // multi-GPU run has not validated it.)
+  // Decomposed mesh (TEAM kernels): flat all-to-all arrival, no last
+  // arriver, no mailbox round trip, no broadcast.  Thread 0 of every block
+  // stores the block's partial sums into EVERY rank's team-partials buffer
+  // (peer memory: NVLink across devices) and then arrives once on every
+  // rank's 64-bit arrival counter after one release fence at the team's
+  // scope (system scope across devices: the fence also orders the block's
+  // halo stores of the pass, observed by thread 0 through the block barrier).  Each
+  // block then waits on its OWN rank's counter for the P x G arrivals of
+  // this round and sums the partials itself: per rank, lane-strided over
+  // that rank's blocks and a shuffle tree, then the ranks in order — the same
+  // sum the per-rank last arriver + rank-order mailbox combine formed, on
+  // every block of every rank.  Rounds and arrivals are counted across
+  // launches (the rank's completed rounds and the arrivals they took live in
+  // its comm area: the CG and BiCGStab grids differ in size), so a fast
+  // peer's arrivals for the next launch are never lost to a counter reset; buffers
+  // alternate by round parity (a block writes round k+2 only after round
+  // k+1 completed everywhere, i.e. after every block read round k).  Every
+  // rank of a team runs the same grid size (same device type, same share).
   (void)sends;  // every block of a team holds send rows (grid-strided rows)
+  unsigned long long& s_base = s_team_round0;
+  unsigned long long& s_abase = s_team_arrive0;
   block_reduce<M>(v, smem);
   volatile unsigned* vabort = sync + 2;
-  double* bcast = reinterpret_cast<double*>(sync + 4);
+  Comm* me = T.comm;
+  const unsigned r = rnd++;
   if (threadIdx.x == 0) {
-    const unsigned gen = ld_relaxed_gpu(sync + 1);
-    s_gen = gen;
-    // partials double-buffered by generation parity: a block can only write
-    // the partial of reduction k+2 after every block passed reduction k+1,
-    // i.e. after every block finished reading the partials of reduction k
-    double* part = partials + size_t(gen & 1u) * kRedStride * gridDim.x;
-#pragma unroll
-    for (int m = 0; m < M; ++m) part[size_t(m) * gridDim.x + blockIdx.x] = v[m];
-    s_last = atom_arrive(sync, SYS) == gridDim.x - 1;  // system scope in a multi-device team
-  }
-  __syncthreads();
-  const unsigned gen = s_gen;
-  const double* part = partials + size_t(gen & 1u) * kRedStride * gridDim.x;
-  if (s_last) {
-    if (!teamed) {
-      if (threadIdx.x == 0) {
-        sync[0] = 0u;  // reset arrivals; ordered before the release below
-        red_release_add(sync + 1, false);
-      }
-    } else if (warp == 0) {
-      // decomposed mesh: this rank's sum goes through the peer mailboxes
-      double r[M];
-#pragma unroll
-      for (int m = 0; m < M; ++m) {
-        double x = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(part + size_t(m) * gridDim.x + b);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-        r[m] = x;
-      }
-      if (lane == 0) {
-        const bool ok = OOL ? team_exchange_ool<M>(T, r, RED_SUM) : team_exchange<M>(T, r, RED_SUM);
-        if (!ok) *vabort = 1u;
-#pragma unroll
-        for (int m = 0; m < M; ++m) __stcg(bcast + m, r[m]);
-        sync[0] = 0u;
-        red_release_add(sync + 1, false);  // the waiters are on this device
-      }
+    if (r == 0) {  // rounds and arrivals of the earlier launches
+      s_base = me->tr_round;
+      s_abase = me->tr_base;
     }
-  } else if (threadIdx.x == 0) {
+    const unsigned long long round = s_base + r;
+    const unsigned long long per_round = (unsigned long long)(T.size) * gridDim.x;
+    const int par = int(round & 1ull);
+#pragma unroll 1
+    for (int q = 0; q < T.size; ++q) {
+      double* part = team_part(T.peer_comm[q]) + team_part_index(par, T.rank, 0, blockIdx.x);
+#pragma unroll
+      for (int m = 0; m < M; ++m) part[size_t(m) * kTeamGridMax] = v[m];
+    }
+    // one release fence, then relaxed arrivals (a release pattern for every
+    // counter: one system-scope fence per block and reduction instead of P)
+    if (SYS)
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#pragma unroll 1
+    for (int q = 0; q < T.size; ++q) {
+      unsigned long long* ctr = &T.peer_comm[q]->tr_arrive;
+      if (SYS)
+        asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+      else
+        asm volatile("red.relaxed.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    }
+    const unsigned long long target = s_abase + (r + 1ull) * per_round;
     const uint64_t t0 = global_ns();
     int spins = 0;
-    while (ld_relaxed_gpu(sync + 1) == gen) {
+    for (;;) {
+      unsigned long long seen;
+      if (SYS)
+        asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(seen) : "l"(&me->tr_arrive) : "memory");
+      else
+        asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(seen) : "l"(&me->tr_arrive) : "memory");
+      if (seen >= target) break;
       if (*vabort) break;
       if (++spins > 64) __nanosleep(32);
-      if ((spins & 1023) == 0 && global_ns() - t0 > kWatchdogNs + 2000000000ull) {
+      if ((spins & 1023) == 0 && global_ns() - t0 > kWatchdogNs) {
+        // diagnostics for the host (team_timeout_error): the round waited
+        // for and the arrivals seen
+        me->pad[0] = target;
+        me->pad[1] = seen;
+        me->pad[6] = kReduceTimeoutMark;
         atomicExch(sync + 2, 1u);
         break;
       }
     }
-  }
-  if (threadIdx.x == 0) {
-    // acquire before reading results: the relaxed load that observed the
-    // new generation (or the last arriver's own release) + fence.acq_rel
-    // is an acquire pattern (and invalidates this SM's L1)
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    // acquire: one acquire load of the counter whose value is used (ptxas
+    // keeps it; the partials and the peers' halo stores are then current,
+    // L1 invalidated) instead of a full fence after the relaxed polls
+    {
+      unsigned long long seen2;
+      if (SYS)
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(seen2) : "l"(&me->tr_arrive) : "memory");
+      else
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(seen2) : "l"(&me->tr_arrive) : "memory");
+      if (seen2 < target) atomicExch(sync + 2, 1u);  // cannot happen: counters only grow
+    }
     s_ok = *vabort == 0;
-    if (teamed) {
-#pragma unroll
-      for (int m = 0; m < M; ++m) smem[32 * M + m] = __ldcg(bcast + m);
+    // block 0 records the round for the next launch (every block read the
+    // base before its first arrival, and round r completed only after
+    // every block arrived)
+    if (blockIdx.x == 0) {
+      me->tr_round = round + 1ull;
+      me->tr_base = target;
     }
   }
   __syncthreads();
-  if (!teamed && warp == 0) {
-    // single device: every block sums the partials itself, in the same
-    // fixed order (lane-strided over blocks, then a shuffle tree)
+  if (warp == 0) {
+    const int par = int((s_base + r) & 1ull);
+    const double* part = team_part(me);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-      double x = 0.0;
-      for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(part + size_t(m) * gridDim.x + b);
+      double acc = 0.0;
+      for (int q = 0; q < T.size; ++q) {
+        const double* pq = part + team_part_index(par, q, m, 0);
+        double x = 0.0;
+        for (int b = lane; b < (int)gridDim.x; b += 32) x += __ldcg(pq + b);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-      if (lane == 0) smem[32 * M + m] = x;
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        acc = q == 0 ? x : acc + x;  // rank order, as the mailbox combine
+      }
+      if (lane == 0) smem[32 * M + m] = acc;
     }
-    __syncwarp();
   }
-  if (!teamed) __syncthreads();
+  __syncthreads();
 #pragma unroll
   for (int m = 0; m < M; ++m) v[m] = smem[32 * M + m];
   const bool ok = s_ok != 0;

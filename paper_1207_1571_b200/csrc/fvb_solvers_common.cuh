@@ -90,6 +90,7 @@ int coop_blocks(Ctx* c, K kernel, int threads, int max_per_sm, int* blocks) {
   if (!c->teamed() && c->nr <= kSingleBlockRowsPerThread * threads) b = 1;
   if (c->solver_max_blocks > 0 && b > c->solver_max_blocks) b = c->solver_max_blocks;
   if (b > int(kStepPartials / (2 * kRedStride))) b = int(kStepPartials / (2 * kRedStride));
+  if (c->teamed() && b > kTeamGridMax) b = kTeamGridMax;  // team-partials buffer (team_reduce)
   *blocks = b < 1 ? 1 : b;
   return FVB_OK;
 }

@@ -55,8 +55,12 @@ int team_timeout_error(Ctx* c) {
   int o = 0;
   for (int q = 0; q < c->team.size && q < kMaxTeam; ++q)
     o += snprintf(peers + o, sizeof peers - o, "%s%llu", q ? "," : "", seq[q]);
-  fvb_set_error("team sync timed out (rank %d of %d): a peer did not arrive (waited for epoch "
-                "%llu; peer epochs now %s)", c->team.rank, c->team.size, d[0], peers);
+  if (d[6] == kReduceTimeoutMark)
+    fvb_set_error("team solver reduction timed out (rank %d of %d): a peer did not arrive "
+                  "(waited for %llu block arrivals, saw %llu)", c->team.rank, c->team.size, d[0], d[1]);
+  else
+    fvb_set_error("team sync timed out (rank %d of %d): a peer did not arrive (waited for epoch "
+                  "%llu; peer epochs now %s)", c->team.rank, c->team.size, d[0], peers);
   return FVB_E_TIMEOUT;
 }
 
