@@ -519,32 +519,9 @@ __device__ bool team_exchange(const TeamView& T, double (&v)[M], int op) {
   return true;
 }
 
-// Out-of-line copy for kernels whose hot loops are register-bound (k_cg):
-// keeps the mailbox code's registers out of the caller's allocation
-// (measured: CG iteration at 2.1M rows 64.1 -> 62.2 us).  The BiCGStab
-// kernels keep the inline copy (out of line they copy the TeamView to local
-// memory around every call and lose more than they gain).
-template <int M>
-__device__ __noinline__ bool team_exchange_ool(const TeamView& T, double (&v)[M], int op) {
-  return team_exchange<M>(T, v, op);
-}
-
-// Scoped atomics / loads of the grid barrier.  Arrival is an acq_rel
-// atomic (release orders this block's partials and stores; the returned
-// count tells the last arriver, whose acquire makes every partial visible);
-// the release of the generation word orders the broadcast; waiters poll
-// relaxed and finish with one acquire load (which also invalidates this
-// SM's L1, so stale lines of the previous pass are never read).  Scope is
-// the GPU, or the system when the mesh is decomposed over several devices
-// (halo stores to peers must be ordered before the peers' mailbox flags).
-__device__ __forceinline__ unsigned atom_arrive(unsigned* p, bool sys) {
-  unsigned o;
-  if (sys)
-    asm volatile("atom.acq_rel.sys.global.add.u32 %0, [%1], 1;" : "=r"(o) : "l"(p) : "memory");
-  else
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(o) : "l"(p) : "memory");
-  return o;
-}
+// Scoped atomics / loads of the single-device grid barrier: arrival is a
+// release add on a monotonic counter, waiters poll relaxed and finish with
+// a fence (an acquire pattern that also invalidates this SM's L1).
 __device__ __forceinline__ void red_release_add(unsigned* p, bool sys) {
   if (sys)
     asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
@@ -556,21 +533,15 @@ __device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
 
 // Grid(+team)-wide deterministic sum of M doubles for co-resident
 // (cooperatively launched) grids.  v holds each thread's partial sums on
 // entry and the global sums on exit, bit-identical in every thread of every
-// block of every rank.  Block partials are summed by the last block to
-// arrive in a fixed order (lane-strided over blocks, then a shuffle tree),
-// the team combine goes through the peer mailboxes, and the result is
-// broadcast through the sync area.  sync words: [0] arrivals, [1]
-// generation, [2] abort flag, [4..) broadcast doubles.  The barrier also
-// orders every halo store issued before it.  Returns false on watchdog.
+// block of every rank: every block sums all block partials itself in a
+// fixed order (lane-strided over blocks, then a shuffle tree; per rank and
+// then in rank order when the mesh is decomposed).  sync words: [0]
+// arrivals (single device), [2] abort flag.  The barrier also orders every
+// halo store issued before it.  Returns false on watchdog.
 // Partials of consecutive reductions alternate between two buffers of
 // kRedStride x gridDim.x doubles.  The buffer stride must not depend on M:
 // with a stride of M x gridDim.x, a fast block writing the partials of
@@ -630,6 +601,8 @@ static __shared__ unsigned long long s_team_arrive0;
 // CLUSTER: the kernel runs as one thread-block cluster (cluster_reduce).
 // SYS: a team over several devices (compile-time, so the single-device and
 // co-resident team kernels carry no system-scope code).
+// OOL: unused since the team path stopped going through the mailboxes
+// (kept so the call sites read the same).
 // BLOCK: the kernel is a single-block solver (a block may be one of several
 // independent solves of a launch), whose block barrier is the grid barrier.
 template <int M, bool OOL = false, bool TEAM = true, bool CLUSTER = false, bool SYS = false,
