@@ -517,17 +517,26 @@ static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
     return sc ? smem_launch(c, k_cg<5, 1024, 1, 1, 0, false, false, true>, prm, 1024, bytes)
               : smem_launch(c, k_cg<5, 1024, 1, 0, 0, false, false, true>, prm, 1024, bytes);
   }
+  // one-cluster CG: 512 threads per CTA (about 2 rows per thread on the
+  // cluster's range): cheaper block barriers in the two reductions per
+  // iteration than with 1024 — 5.5 vs 6.6 us per iteration at 13.8k rows,
+  // 7.7 vs 8.2 at 32.8k, 8.9 vs 10.6 at 39.3k; 256 is slower again
+  // (profiles/r02_small.md)
+#ifndef FVB_DIAG_CLUSTER_THREADS  // diagnostic builds: threads per cluster CTA
+#define FVB_DIAG_CLUSTER_THREADS 512
+#endif
+  constexpr int CLT = FVB_DIAG_CLUSTER_THREADS;
   if (!TEAM && (c->k == 7 || c->k == 5)) {
-    const int want = cluster_want(c, 1024);
-    const int nb = want ? (c->k == 7 ? cluster_blocks(c, k_cg<7, 1024, 1, 1, 1, false, true>, 1024, want)
-                                     : cluster_blocks(c, k_cg<5, 1024, 1, 1, 0, false, true>, 1024, want))
+    const int want = cluster_want(c, CLT);
+    const int nb = want ? (c->k == 7 ? cluster_blocks(c, k_cg<7, CLT, 1, 1, 1, false, true>, CLT, want)
+                                     : cluster_blocks(c, k_cg<5, CLT, 1, 1, 0, false, true>, CLT, want))
                         : 0;
     if (nb >= 2) {
       if (c->k == 7)
-        return sc ? cluster_launch(c, k_cg<7, 1024, 1, 1, 1, false, true>, prm, 1024, nb)
-                  : cluster_launch(c, k_cg<7, 1024, 1, 0, 1, false, true>, prm, 1024, nb);
-      return sc ? cluster_launch(c, k_cg<5, 1024, 1, 1, 0, false, true>, prm, 1024, nb)
-                : cluster_launch(c, k_cg<5, 1024, 1, 0, 0, false, true>, prm, 1024, nb);
+        return sc ? cluster_launch(c, k_cg<7, CLT, 1, 1, 1, false, true>, prm, CLT, nb)
+                  : cluster_launch(c, k_cg<7, CLT, 1, 0, 1, false, true>, prm, CLT, nb);
+      return sc ? cluster_launch(c, k_cg<5, CLT, 1, 1, 0, false, true>, prm, CLT, nb)
+                : cluster_launch(c, k_cg<5, CLT, 1, 0, 0, false, true>, prm, CLT, nb);
     }
   }
   switch (c->k) {
