@@ -539,6 +539,16 @@ static int cg_launch(Ctx* c, CgParams& prm, bool sc) {
                 : cluster_launch(c, k_cg<5, CLT, 1, 0, 0, false, true>, prm, CLT, nb);
     }
   }
+#ifdef FVB_DIAG_GRID_THREADS  // diagnostic builds: threads per block of the single-domain grid
+  if (!TEAM && (c->k == 5 || c->k == 7)) {
+    constexpr int GT = FVB_DIAG_GRID_THREADS;
+    if (c->k == 5)
+      return sc ? coop_launch(c, k_cg<5, GT, 1, 1, 0>, prm, GT, 1)
+                : coop_launch(c, k_cg<5, GT, 1, 0, 0>, prm, GT, 1);
+    return sc ? coop_launch(c, k_cg<7, GT, 1, 1, 1>, prm, GT, 1)
+              : coop_launch(c, k_cg<7, GT, 1, 0, 1>, prm, GT, 1);
+  }
+#endif
   switch (c->k) {
     case 5:
       if (sc) return coop_launch(c, k_cg<5, 1024, 1, 1, 0, TEAM, false, false, SYS>, prm, 1024, 1);
