@@ -96,3 +96,40 @@ def test_errors():
     m.points[:, 0] = 0.0  # flatten: every x-normal face degenerates
     with pytest.raises(MeshError, match="degenerate"):
         pmesh.compute_geometry(m)
+
+
+def test_face_triangles_close_the_volume():
+    """mesh._face_triangles (reference mesh.py:154-170): the fan triangles of
+    a warped hexahedron reproduce the native geometry's cell volume through
+    the divergence identity (the reference's test_mesh.py check)."""
+    from paper_1207_1571_b200.mesh import Mesh, Patch
+
+    corners = np.array([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0],
+                        [0, 0, 1], [1, 0, 1], [1, 1, 1], [0, 1, 1]], dtype=float)
+    loops = [[0, 3, 2, 1], [4, 5, 6, 7], [0, 4, 7, 3], [1, 2, 6, 5], [0, 1, 5, 4], [3, 7, 6, 2]]
+    rng = np.random.default_rng(3)
+    for _ in range(10):
+        pts = corners + rng.uniform(-0.15, 0.15, size=(8, 3))
+        m = Mesh(points=pts, face_points=np.concatenate(loops).astype(np.int64),
+                 face_offsets=np.arange(0, 25, 4, dtype=np.int64), owner=np.zeros(6, dtype=np.int64),
+                 neighbour=np.zeros(0, dtype=np.int64), patches=[Patch("walls", "wall", 0, 6)],
+                 n_cells=1)
+        m.validate()
+        geo = pmesh.compute_geometry(m)
+        a, b, seed, face = pmesh._face_triangles(m)
+        assert a.shape == b.shape == seed.shape == (24, 3) and list(face) == sorted(face)
+        tri_s = 0.5 * np.cross(b - a, seed - a)
+        vol = np.einsum("ij,ij->i", (a + b + seed) / 3.0, tri_s).sum() / 3.0
+        assert geo.cell_volume[0] == pytest.approx(vol, rel=1e-12)
+
+
+def test_jacobi_apply():
+    """linsolve.jacobi_apply (reference linsolve.py:82-87): r / D, and the
+    solvers' zero-diagonal message."""
+    from paper_1207_1571_b200.linsolve import SolverError, jacobi_apply
+
+    d = np.array([2.0, 4.0, 0.5])
+    r = np.array([1.0, -2.0, 3.0])
+    assert np.array_equal(jacobi_apply(d, r), r / d)
+    with pytest.raises(SolverError, match="zero diagonal at row 1"):
+        jacobi_apply(np.array([1.0, 0.0, 0.0]), np.ones(3))
