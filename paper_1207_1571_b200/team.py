@@ -123,12 +123,15 @@ class _LocalField:
         self.rank = field.rank
 
 
-def _scope(same_device):
-    """System-scope ordering unless every rank shares one device;
-    FVB_TEAM_SCOPE=sys|gpu overrides (experiments)."""
-    env = os.environ.get("FVB_TEAM_SCOPE")
-    if env in ("sys", "gpu"):
-        return 1 if env == "sys" else 0
+def _scope(same_device, scope=None):
+    """System-scope ordering unless every rank shares one device; `scope`
+    ("sys" / "gpu") forces one (DecomposedRun: the system-scope kernels a
+    multi-GPU team runs, exercised on one device by tests and
+    tools/team_bench.py)."""
+    if scope is not None:
+        if scope not in ("sys", "gpu"):
+            raise ValueError(f"scope must be 'sys' or 'gpu', not {scope!r}")
+        return 1 if scope == "sys" else 0
     return 0 if same_device else 1
 
 
@@ -201,7 +204,7 @@ class _TeamRunBase:
 class DecomposedRun(_TeamRunBase):
     """All ranks of a decomposition in this process (one thread per rank)."""
 
-    def __init__(self, case, cfg, nparts, devices=None, part=None):
+    def __init__(self, case, cfg, nparts, devices=None, part=None, scope=None):
         self._init_common(case, cfg)
         mesh = case.mesh
         self.geom = compute_geometry(mesh)
@@ -226,7 +229,7 @@ class DecomposedRun(_TeamRunBase):
         bases = [e[0] for e in ex]
         ncs = [e[1] for e in ex]
         same_device = len(set(devices)) == 1
-        scope = _scope(same_device)
+        scope = _scope(same_device, scope)
         for m in self.members:  # allocations + copies: no team sync inside
             _lib.check(m.attach(bases, ncs))
             _lib.check(_lib.lib.fvb_team_set_scope(m.ctx.h, scope))

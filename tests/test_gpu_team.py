@@ -30,8 +30,8 @@ def _single(case, cfg, steps):
     return st
 
 
-def _team(case, cfg, steps, nparts):
-    run = DecomposedRun(case, cfg, nparts)
+def _team(case, cfg, steps, nparts, scope=None):
+    run = DecomposedRun(case, cfg, nparts, scope=scope)
     for _ in range(steps):
         if cfg.algorithm == "piso":
             run.piso_time_step(cfg)
@@ -126,18 +126,17 @@ def test_ipc_team_two_processes_one_device():
 
 
 @pytest.mark.parametrize("nparts", [2, 4])
-def test_team_system_scope_kernels(nparts, monkeypatch):
-    # the kernels a team over several GPUs uses (system-scope arrivals and
-    # mailbox fences, the SYS instantiations), forced on one device with
-    # FVB_TEAM_SCOPE=sys: same results as the single-domain run under the
-    # parity rules
-    monkeypatch.setenv("FVB_TEAM_SCOPE", "sys")
+def test_team_system_scope_kernels(nparts):
+    # the kernels a team over several GPUs uses (system-scope release fences
+    # and acquires, the SYS instantiations), forced on one device with
+    # scope="sys": same results as the single-domain run under the parity
+    # rules
     case = cases.gen_cavity(12)
     case.config.algorithm, case.config.dt = "piso", 0.1 / 12
     case.config.cg_tol, case.config.bicgstab_tol, case.config.max_iters = 1e-13, 1e-10, 20000
     cfg = CouplingConfig.from_case_config(case.config)
     st = _single(case, cfg, 2)
-    run = _team(case, cfg, 2, nparts)
+    run = _team(case, cfg, 2, nparts, scope="sys")
     u, p, flux = run.gather()
     assert rel(u, st.u.values) < 1e-9 and rel(p, st.p.values) < 1e-9 and rel(flux, st.flux) < 1e-9
     for a, b in zip(run.residual_log, st.residual_log):

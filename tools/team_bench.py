@@ -5,7 +5,8 @@ ranks on one B200 the per-rank bandwidth is 1/P of the device, so the ideal
 is equal step time for every P; the difference is the cost of the team
 machinery (halo stores, peer-mailbox reductions, halo syncs) without the
 NVLink latency of a real multi-GPU run.
-Usage: python tools/team_bench.py N P [P ...]"""
+Usage: python tools/team_bench.py N P [P ...] [sys]   (sys: force the
+system-scope kernels of a multi-GPU team; FVB_TEAM_SCOPE=sys does the same)"""
 import json, os, sys, time
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 from paper_1207_1571_b200 import cases
@@ -13,11 +14,12 @@ from paper_1207_1571_b200.coupling import CouplingConfig
 from paper_1207_1571_b200.team import DecomposedRun
 
 n = int(sys.argv[1])
-for P in [int(x) for x in sys.argv[2:]]:
+scope = "sys" if ("sys" in sys.argv[2:] or os.environ.get("FVB_TEAM_SCOPE") == "sys") else None
+for P in [int(x) for x in sys.argv[2:] if x != "sys"]:
     case = cases.gen_cavity(n)
     case.config.algorithm, case.config.dt = "piso", 0.1 / n
     cfg = CouplingConfig.from_case_config(case.config)
-    run = DecomposedRun(case, cfg, P)
+    run = DecomposedRun(case, cfg, P, scope=scope)
     for _ in range(2):
         run.piso_time_step(cfg)
     t0 = time.perf_counter()
