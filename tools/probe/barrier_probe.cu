@@ -10,6 +10,10 @@
 //   D  last arriver sums and publishes; the others poll a generation word
 //   E  A without the block reduction (thread 0's own value is the partial)
 //   F  E without the partial sums (the barrier alone)
+//   H  A with every partial load of both values issued before the sums
+//   I  A with the partial loads k-outer / value-inner over a fixed 16-step
+//      lane stride (predicated), accumulated in the same order
+//   J  I with one warp per value (warp m sums value m)
 //   G  per-block round tags instead of one counter: each block stores its
 //      partials and then its tag (release); warp 0 of every block polls the
 //      tags lane-strided, fences, and sums the partials (no atomics)
@@ -133,7 +137,54 @@ __global__ void __launch_bounds__(1024, 1) k_probe(int rounds, unsigned* ctr, do
       asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     __syncthreads();
-    if (VAR != 5 && warp == 0)
+    if (VAR == 7 && warp == 0) {
+      constexpr int NB = 5;  // ceil(148 / 32)
+      double xs[M][NB];
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const int b = lane + 32 * k;
+          xs[m][k] = b < G ? __ldcg(pp + m * G + b) : 0.0;
+        }
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double x = 0.0;
+#pragma unroll
+        for (int k = 0; k < NB; ++k) x += xs[m][k];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) sm[32 * M + m] = x;
+      }
+    } else if (VAR == 8 && warp == 0) {
+      double xm[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) xm[m] = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int b = lane + 32 * k;
+        if (b < G) {
+#pragma unroll
+          for (int m = 0; m < M; ++m) xm[m] += __ldcg(pp + m * G + b);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        double x = xm[m];
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) sm[32 * M + m] = x;
+      }
+    } else if (VAR == 9) {
+      if (warp < M) {
+        double x = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int b = lane + 32 * k;
+          if (b < G) x += __ldcg(pp + warp * G + b);
+        }
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) sm[32 * M + warp] = x;
+      }
+    } else if (VAR != 5 && warp == 0)
       for (int m = 0; m < M; ++m) {
         double x = 0.0;
         for (int b = lane; b < G; b += 32) x += __ldcg(pp + m * G + b);
@@ -191,11 +242,12 @@ int main() {
   cudaMalloc(&out, 64 * sizeof(double));
   const int R = 4000;
   for (int rep = 0; rep < 2; ++rep) {
-    printf("blocks %d rounds %d (us per reduction): A %.3f  B %.3f  C %.3f  D %.3f  E %.3f  F %.3f  G %.3f\n", sms, R,
+    printf("blocks %d rounds %d (us per reduction): A %.3f  B %.3f  C %.3f  D %.3f  E %.3f  F %.3f  G %.3f  H %.3f  I %.3f  J %.3f\n", sms, R,
            1e3f * run<0>(sms, R, ctr, part, out) / R, 1e3f * run<1>(sms, R, ctr, part, out) / R,
            1e3f * run<2>(sms & ~1, R, ctr, part, out) / R, 1e3f * run<3>(sms, R, ctr, part, out) / R,
            1e3f * run<4>(sms, R, ctr, part, out) / R, 1e3f * run<5>(sms, R, ctr, part, out) / R,
-           1e3f * run<6>(sms, R, ctr, part, out) / R);
+           1e3f * run<6>(sms, R, ctr, part, out) / R, 1e3f * run<7>(sms, R, ctr, part, out) / R,
+           1e3f * run<8>(sms, R, ctr, part, out) / R, 1e3f * run<9>(sms, R, ctr, part, out) / R);
   }
   return 0;
 }
