@@ -725,7 +725,18 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
       s_ok = *vabort == 0;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (M > 3) {
+      // many values (BiCGStab batches): one warp per value, in parallel
+      if (warp < M) {
+        const int G = int(gridDim.x);
+        const double* pm = part + size_t(warp) * gridDim.x;
+        double x = 0.0;
+        for (int b = lane; b < G; b += 32) x += __ldcg(pm + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) smem[32 * M + warp] = x;
+      }
+    } else if (warp == 0) {
       double xs[M];
       lane_sums<M>(part, gridDim.x, int(gridDim.x), lane, xs);
 #pragma unroll
@@ -842,25 +853,22 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
     }
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp < M) {
+    // one warp per value (in parallel): per rank lane-strided over that
+    // rank's blocks and a shuffle tree, then the ranks in order
     const int par = int((s_base + r) & 1ull);
     const double* part = team_part(me);
-    double acc[M];
+    const int G = int(gridDim.x);
+    double acc = 0.0;
     for (int q = 0; q < T.size; ++q) {
-      double xs[M];
-      lane_sums<M>(part + team_part_index(par, q, 0, 0), kTeamGridMax, int(gridDim.x), lane, xs);
+      const double* pq = part + team_part_index(par, q, warp, 0);
+      double x = 0.0;
+      for (int b = lane; b < G; b += 32) x += __ldcg(pq + b);
 #pragma unroll
-      for (int m = 0; m < M; ++m) {
-        double x = xs[m];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-        acc[m] = q == 0 ? x : acc[m] + x;  // rank order, as the mailbox combine
-      }
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+      acc = q == 0 ? x : acc + x;  // rank order, as the mailbox combine
     }
-    if (lane == 0) {
-#pragma unroll
-      for (int m = 0; m < M; ++m) smem[32 * M + m] = acc[m];
-    }
+    if (lane == 0) smem[32 * M + warp] = acc;
   }
   __syncthreads();
 #pragma unroll
