@@ -1,5 +1,5 @@
 """Drop-in conformance: the reference's own unit tests (fvflow
-pkg/tests/test_{mesh,sparse,linsolve,fvm,coupling}.py) run UNMODIFIED
+pkg/tests/test_{mesh,sparse,linsolve,fvm,coupling,report,acceptance}.py) run UNMODIFIED
 against this package, with `fvflow.<module>` aliased to
 `paper_1207_1571_b200.<module>` (tools/fvflow_alias.py; VERDICT r01
 "missing" item 6).
@@ -24,7 +24,7 @@ ROOT = os.path.dirname(HERE)
 SRC = "/root/reference/pkg/tests"
 DST = os.path.join(ROOT, "baseline", "_ref_tests")
 FILES = ("conftest.py", "helpers_mms.py", "test_mesh.py", "test_sparse.py", "test_linsolve.py",
-         "test_fvm.py", "test_coupling.py")
+         "test_fvm.py", "test_coupling.py", "test_report.py", "test_acceptance.py")
 
 
 def stage():
