@@ -725,8 +725,8 @@ __device__ __forceinline__ bool team_reduce(const TeamView& T, unsigned* sync,
       s_ok = *vabort == 0;
     }
     __syncthreads();
-    if (M > 3) {
-      // many values (BiCGStab batches): one warp per value, in parallel
+    if (M > 1) {
+      // several values: one warp per value, in parallel
       if (warp < M) {
         const int G = int(gridDim.x);
         const double* pm = part + size_t(warp) * gridDim.x;
